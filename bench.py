@@ -1,0 +1,481 @@
+#!/usr/bin/env python
+"""Benchmark: Sauvola binarization Mpixel/s on 1..8 B200 (+ % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c4|c3|c5|c2|c1] [--scaling weak|strong]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (default): BASELINE config 4 -- a 16384x16384 synthetic gray page,
+Sauvola W=127 k=0.34 R=128, split in row bands across ranks with the 63-row
+halos exchanged point-to-point (NCCL send/recv over NVLink) every step.
+``--scaling weak`` (default): every rank owns one full 16384x16384 band of a
+(16384*N)-row page, so per-GPU work is fixed; ``strong`` splits the one
+16384x16384 page N ways.  One step = halo exchange + one pass of the fused
+sliding-sum binarization kernel over the rank's band.
+
+Prints ONE JSON line (rank 0).  ``value`` is whole-job Mpixel/s with inputs
+resident in HBM, timed with CUDA events (max over ranks); ``e2e`` is the
+same metric through the public API with pinned host buffers and the H2D/D2H
+copies inside the timed region; ``roofline`` is the kernel's achieved
+algorithmic bandwidth (2 B/px) vs the measured HBM copy peak; ``cpu_baseline``
+is the CPU oracle port (oracle/, a C restatement of the reference's integral
+engine) on the box's host cores on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Sauvola binarization Mpixel/s"
+UNIT = "Mpixel/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["c4", "c3", "c5", "c2", "c1"], default="c4")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--window", type=int, default=None, help="override W (c5 sweep point)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid: str | None):
+        self.lines = []
+        cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+               "-lms", "200"]
+        if uuid:
+            cmd += ["-i", uuid]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workloads
+
+def workload(cfg_name, world, rank, scaling, window):
+    """-> dict(kind, host arrays for this rank, params, pixels per rank, description)."""
+    import numpy as np
+
+    from paper_1210_3165_b200 import workloads as wl
+    cfg = wl.CONFIGS[cfg_name]
+    win = window or cfg.windows[0]
+    if cfg_name in ("c4", "c5", "c1"):
+        img = {"c4": wl.c4_image, "c5": wl.c5_image, "c1": wl.c1_image}[cfg_name]()
+        H, Wd = img.shape
+        r = win // 2
+        if scaling == "weak":
+            # page = `world` copies of the image stacked vertically; rank i owns copy i
+            rows = H * world
+            y0, y1 = H * rank, H * (rank + 1)
+            top = img[H - r:] if rank > 0 else img[:0]
+            bot = img[:r] if rank < world - 1 else img[:0]
+            band = img
+        else:
+            rows = H
+            y0, y1 = H * rank // world, H * (rank + 1) // world
+            top, band, bot = img[max(y0 - r, 0):y0], img[y0:y1], img[y1:min(y1 + r, H)]
+        host_halo = np.ascontiguousarray(np.concatenate([top, band, bot]))
+        return dict(kind="rowband", band=np.ascontiguousarray(band), halo=host_halo,
+                    a=y0 - len(top), rows=rows, y0=y0, y1=y1, cols=Wd, win=win,
+                    method=cfg.method, k=cfg.k, r=cfg.r, px_rank=(y1 - y0) * Wd,
+                    desc=(f"{cfg_name}: {H}x{Wd} gray page(s), {cfg.method} W={win} k={cfg.k} "
+                          f"R={cfg.r}; {'weak' if scaling == 'weak' else 'strong'} row-band "
+                          f"split over {world} GPU(s), {r}-row halos via NCCL P2P"),
+                    shape=[rows, Wd])
+    if cfg_name == "c3":
+        n_total = 64 * (world if scaling == "weak" else 1)
+        per = [i for i in range(n_total) if (i * world) // n_total == rank]
+        imgs = np.stack([wl.c3_image(i % 64) for i in per])
+        return dict(kind="batch", stack=imgs, win=win, method=cfg.method, k=cfg.k, r=cfg.r,
+                    px_rank=imgs.size, shape=[n_total, 2048, 2048],
+                    desc=f"c3: {n_total} x 2048x2048 gray, niblack W={win} k={cfg.k}, by image")
+    if cfg_name == "c2":
+        rgb = wl.c2_rgb()
+        return dict(kind="rgb", rgb=rgb, win=win, method=cfg.method, k=cfg.k, r=cfg.r,
+                    px_rank=rgb.shape[0] * rgb.shape[1], shape=list(rgb.shape),
+                    desc=f"c2: 3508x2480 RGB page, fused to_gray + sauvola W={win}")
+    raise ValueError(cfg_name)
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1210_3165_b200 import distributed as D
+    from paper_1210_3165_b200 import engine
+    import paper_1210_3165_b200 as dt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = workload(a.config, world, rank, a.scaling, a.window)
+    props = torch.cuda.get_device_properties(dev)
+    l2 = int(getattr(props, "L2_cache_size", 126 * 2**20))
+    stream = torch.cuda.current_stream()
+
+    # ---- device-resident buffers, rotated so the per-step footprint defeats L2
+    if w["kind"] == "rowband":
+        band = torch.from_numpy(w["band"]).to(dev)
+        per_step_bytes = 2 * band.numel()
+        nrot = max(1, -(-2 * l2 // per_step_bytes))
+        bands = [band] + [band.clone() for _ in range(nrot - 1)]
+        outs = [torch.empty_like(band) for _ in range(nrot)]
+        r = w["win"] // 2
+        ha, hz = D.halo_bounds(w["rows"], w["y0"], w["y1"], r)
+        halo_bufs = [torch.empty((hz - ha,) + tuple(band.shape[1:]), dtype=torch.uint8,
+                                 device=dev) for _ in range(nrot)] if world > 1 else None
+        launches_per_step = 1
+
+        def kernel(i):
+            if world > 1:
+                buf, a0 = D.exchange_halos(bands[i], w["rows"], r, out=halo_bufs[i])
+            else:
+                buf, a0 = bands[i], w["y0"]
+            return buf, a0
+
+        def step(i, ev=None):
+            j = i % nrot
+            buf, a0 = kernel(j)
+            if ev is not None:
+                ev[0].record(stream)
+            engine.binarize_band(buf, a0, w["rows"], w["y0"], w["y1"], w["win"], w["method"],
+                                 w["k"], w["r"], out=outs[j])
+            if ev is not None:
+                ev[1].record(stream)
+    elif w["kind"] == "batch":
+        stack = torch.from_numpy(w["stack"]).to(dev)
+        per_step_bytes = 2 * stack.numel()
+        nrot = max(1, -(-2 * l2 // per_step_bytes))
+        stacks = [stack] + [stack.clone() for _ in range(nrot - 1)]
+        outs = [torch.empty_like(stack) for _ in range(nrot)]
+        launches_per_step = 1
+
+        def step(i, ev=None):
+            j = i % nrot
+            if ev is not None:
+                ev[0].record(stream)
+            engine.binarize_batch(stacks[j], w["win"], w["method"], w["k"], w["r"], out=outs[j])
+            if ev is not None:
+                ev[1].record(stream)
+    else:  # rgb fused
+        rgb = torch.from_numpy(w["rgb"]).to(dev)
+        per_step_bytes = 4 * rgb.shape[0] * rgb.shape[1]
+        nrot = max(1, -(-2 * l2 // per_step_bytes))
+        rgbs = [rgb] + [rgb.clone() for _ in range(nrot - 1)]
+        launches_per_step = 2
+
+        def step(i, ev=None):
+            j = i % nrot
+            if ev is not None:
+                ev[0].record(stream)
+            engine.rgb_binarize(rgbs[j], w["win"], w["method"], w["k"], w["r"])
+            if ev is not None:
+                ev[1].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for i in range(a.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(a.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(None) if rank == 0 else None
+    barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for i in range(a.steps):
+        step(i, kev[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = t0.elapsed_time(t1) / a.steps
+    kms = statistics.fmean(s.elapsed_time(e) for s, e in kev)
+    if world > 1:
+        t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kms = float(t[0]), float(t[1])
+    total_px = w["px_rank"] * world if a.scaling == "weak" or w["kind"] != "rowband" else (
+        w["shape"][0] * w["shape"][1])
+    if w["kind"] == "batch" and a.scaling == "strong":
+        total_px = int(np.prod(w["shape"]))
+    value = total_px / (ms / 1e3) / 1e6
+
+    # ---- roofline of the dominant kernel (per-launch algorithmic bytes / avg duration)
+    alg_bytes = per_step_bytes
+    peak, peak_kind = measured_peaks()
+    achieved = alg_bytes / (kms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pt = json.load(open(prof))
+            if pt.get("config") == a.config and pt.get("window") == w["win"]:
+                traffic = pt.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, w, world, rank, local, dev, barrier)
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(w, a.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True,
+            "scaling": a.scaling if w["kind"] != "rgb" else "weak",
+            "vs_baseline": None, "dtype": "u8 in/out; int32 sums; f64 epilogue",
+            "data": "synthetic (seeded, paper_1210_3165_b200/workloads.py)",
+            "config": {"workload": w["desc"], "image": w["shape"], "window": w["win"],
+                       "method": w["method"], "k": w["k"], "r": w["r"],
+                       "parallelism": f"{'rowband' if w['kind'] == 'rowband' else 'image'}{world}",
+                       "l2": (f"{nrot} rotating input/output buffer sets, "
+                              f"{nrot * per_step_bytes / 2**20:.0f} MiB per rank >= 2x L2 "
+                              f"({l2 / 2**20:.0f} MiB)")},
+            "kernel_ms": round(kms, 5),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "alg_bytes_per_launch": alg_bytes},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+            "gpu_launches": launches_per_step * a.steps,
+            "gpu": torch.cuda.get_device_name(dev),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(a, w, world, rank, local, dev, barrier):
+    """Public API, pinned host in/out, H2D + kernel + D2H inside the timed region."""
+    import torch
+
+    import paper_1210_3165_b200 as dt
+    from paper_1210_3165_b200 import engine
+
+    stream = torch.cuda.current_stream()
+    if w["kind"] == "rowband":
+        host_in = torch.from_numpy(w["halo"]).pin_memory()
+        host_out = torch.empty((w["y1"] - w["y0"], w["cols"]), dtype=torch.uint8).pin_memory()
+        if world == 1 and w["halo"].shape[0] == w["rows"]:
+            params = dt.BinarizationParams(method=w["method"], engine="integral", window=w["win"],
+                                           r=w["r"], **({"k_sauvola": w["k"]} if w["method"] == "sauvola" else {"k_niblack": w["k"]}))
+
+            def call():
+                dt.binarize(host_in, params, return_tmap=False, out=host_out)
+        else:
+            def call():
+                buf = host_in.to(dev, non_blocking=True)
+                out = engine.binarize_band(buf, w["a"], w["rows"], w["y0"], w["y1"], w["win"],
+                                           w["method"], w["k"], w["r"])
+                host_out.copy_(out, non_blocking=True)
+                stream.synchronize()
+        h2d, d2h = host_in.numel(), host_out.numel()
+    elif w["kind"] == "batch":
+        host_in = torch.from_numpy(w["stack"]).pin_memory()
+        host_out = torch.empty_like(host_in).pin_memory()
+
+        def call():
+            s = host_in.to(dev, non_blocking=True)
+            out = engine.binarize_batch(s, w["win"], w["method"], w["k"], w["r"])
+            host_out.copy_(out, non_blocking=True)
+            stream.synchronize()
+        h2d, d2h = host_in.numel(), host_out.numel()
+    else:
+        host_in = torch.from_numpy(w["rgb"]).pin_memory()
+        host_out = torch.empty(w["rgb"].shape[:2], dtype=torch.uint8).pin_memory()
+
+        def call():
+            s = host_in.to(dev, non_blocking=True)
+            out = engine.rgb_binarize(s, w["win"], w["method"], w["k"], w["r"])
+            host_out.copy_(out, non_blocking=True)
+            stream.synchronize()
+        h2d, d2h = host_in.numel(), host_out.numel()
+    for _ in range(max(1, a.warmup)):
+        call()
+    steps = max(3, a.steps // 2)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for _ in range(steps):
+        call()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    px = w["px_rank"] * world
+    return {"value": round(px / (ms / 1e3) / 1e6, 1), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+            "ms_per_step": round(ms, 4), "steps": steps,
+            "path": "paper_1210_3165_b200.binarize / engine C-ABI calls, pinned host buffers"}
+
+
+# ----------------------------------------------------------------------------- CPU arm
+
+def cpu_sample(w):
+    """Bounded CPU sample of the workload: <= 2048 rows of the band (plus halo rows)."""
+    import numpy as np
+    if w["kind"] == "rowband":
+        img = w["halo"]
+        top = w["y0"] - w["a"]
+        n = min(2048, w["y1"] - w["y0"])
+        r = w["win"] // 2
+        lo, hi = max(top - r, 0), min(top + n + r, img.shape[0])
+        sub = np.ascontiguousarray(img[lo:hi])
+        return sub, n, (top - lo), f"rows [{w['y0']},{w['y0'] + n}) of the band + {r}-row halos"
+    if w["kind"] == "batch":
+        return w["stack"][0], w["stack"][0].shape[0], 0, "1 of the 2048x2048 images"
+    from oracle import to_gray
+    g = to_gray(w["rgb"])
+    return g, g.shape[0], 0, "the full page (gray binarize only)"
+
+
+def cpu_baseline(w, seconds, reps=None):
+    import oracle
+    threads = len(os.sched_getaffinity(0))
+    sub, n, off, desc = cpu_sample(w)
+    px = n * sub.shape[1]
+    times = []
+    t_end = time.perf_counter() + seconds
+    while True:
+        t = time.perf_counter()
+        oracle.binarize(sub, w["win"], w["method"], w["k"], w["r"], tmap=False, threads=threads)
+        times.append(time.perf_counter() - t)
+        if (reps and len(times) >= reps) or (not reps and time.perf_counter() > t_end):
+            break
+    med = statistics.median(times)
+    return {"value": round(px / med / 1e6, 2), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{desc}: {px} px, {len(times)} reps, median {med * 1e3:.1f} ms; "
+                      "C restatement of the reference integral engine (oracle/oracle.c)"}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import oracle
+    w = workload(a.config, 1, 0, a.scaling, a.window)
+    threads = len(os.sched_getaffinity(0))
+    sub, n, off, desc = cpu_sample(w)
+    px = n * sub.shape[1]
+    for _ in range(a.warmup):
+        oracle.binarize(sub, w["win"], w["method"], w["k"], w["r"], tmap=False, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        oracle.binarize(sub, w["win"], w["method"], w["k"], w["r"], tmap=False, threads=threads)
+    dt = (time.perf_counter() - t0) / a.steps
+    v = round(px / dt / 1e6, 2)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(dt * 1e3, 3),
+            "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
+            "dtype": "u8 in/out; int64 sums; f64 epilogue", "data": "synthetic",
+            "config": {"workload": w["desc"], "window": w["win"], "parallelism": f"cpu{threads}"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{desc}: {px} px per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,111 @@
+"""Multi-GPU partitioning of the binarization path (BASELINE.json north_star item 4).
+
+One process per GPU (torchrun), torch.distributed for the plumbing.  Two
+strategies, neither needs a reduction collective:
+
+* by image (config 3): a batch of equally sized pages is split into
+  contiguous shards, one per rank; no communication at all.
+* by row band (config 4): one huge page is split into contiguous row bands;
+  each band needs the r = W//2 rows above and below it, which are exchanged
+  peer-to-peer (NCCL send/recv over NVLink on B200; gloo on CPU in tests)
+  before the band kernel runs.  Window clipping inside the kernel uses GLOBAL
+  row indices, so the stitched bands equal the whole-image result bit for bit.
+
+The band kernel is injectable (``compute``) so the host-side logic (band
+bounds, halo routing, assembly) is exercised on CPU with world_size 2 under
+gloo; the production call is ``engine.binarize_band`` (libdocthresh_b200).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+def band_bounds(rows: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, near-equal row bands: rank i owns [rows*i//world, rows*(i+1)//world)."""
+    return rows * rank // world, rows * (rank + 1) // world
+
+
+def halo_bounds(rows: int, y0: int, y1: int, r: int) -> tuple[int, int]:
+    """Global rows a band [y0, y1) needs for a radius-r window: [max(y0-r,0), min(y1+r,rows))."""
+    return max(y0 - r, 0), min(y1 + r, rows)
+
+
+def shard_bounds(n_items: int, world: int, rank: int) -> tuple[int, int]:
+    return n_items * rank // world, n_items * (rank + 1) // world
+
+
+def halo_plan(rows: int, world: int, r: int):
+    """All (src_rank, dst_rank, g0, g1) transfers: rows [g0, g1) of src's band needed by dst."""
+    plan = []
+    for dst in range(world):
+        y0, y1 = band_bounds(rows, world, dst)
+        a, z = halo_bounds(rows, y0, y1, r)
+        for src in range(world):
+            if src == dst:
+                continue
+            s0, s1 = band_bounds(rows, world, src)
+            for lo, hi in ((a, y0), (y1, z)):
+                g0, g1 = max(lo, s0), min(hi, s1)
+                if g0 < g1:
+                    plan.append((src, dst, g0, g1))
+    return plan
+
+
+def exchange_halos(band: torch.Tensor, rows: int, r: int, group=None,
+                   out: torch.Tensor | None = None) -> tuple[torch.Tensor, int]:
+    """Assemble [halo_top | band | halo_bottom] on this rank.
+
+    ``band`` holds this rank's global rows [y0, y1).  Returns (buffer, a) where
+    buffer holds global rows [a, z).  Transfers are point-to-point (isend /
+    irecv batched), ordered by the stream; no collective reduction.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    y0, y1 = band_bounds(rows, world, rank)
+    a, z = halo_bounds(rows, y0, y1, r)
+    if band.shape[0] != y1 - y0:
+        raise ValueError(f"rows: band has {band.shape[0]} rows, expected {y1 - y0}")
+    if out is None:
+        out = torch.empty((z - a,) + tuple(band.shape[1:]), dtype=band.dtype, device=band.device)
+    out[y0 - a:y1 - a].copy_(band)
+    ops = []
+    for src, dst, g0, g1 in halo_plan(rows, world, r):
+        if dst == rank:
+            ops.append(dist.P2POp(dist.irecv, out[g0 - a:g1 - a], src, group))
+        elif src == rank:
+            ops.append(dist.P2POp(dist.isend, band[g0 - y0:g1 - y0].contiguous(), dst, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out, a
+
+
+def binarize_rowbands(band: torch.Tensor, rows: int, win: int, method: str, k: float,
+                      r: float, group=None, compute: Callable | None = None,
+                      halo_buf: torch.Tensor | None = None, out: torch.Tensor | None = None):
+    """This rank's binarized rows [y0, y1) of a page split in row bands across the group."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    y0, y1 = band_bounds(rows, world, rank)
+    buf, a = exchange_halos(band, rows, win // 2, group, out=halo_buf)
+    if compute is None:
+        from . import engine
+        return engine.binarize_band(buf, a, rows, y0, y1, win, method, k, r, out=out)
+    return compute(buf, a, rows, y0, y1, win, method, k, r)
+
+
+def binarize_images(stack: torch.Tensor, win: int, method: str, k: float, r: float,
+                    group=None, compute: Callable | None = None, out=None):
+    """This rank's shard of an (N, H, W) batch; returns (i0, i1, binary shard)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    i0, i1 = shard_bounds(stack.shape[0], world, rank)
+    shard = stack[i0:i1]
+    if compute is None:
+        from . import engine
+        return i0, i1, engine.binarize_batch(shard, win, method, k, r, out=out)
+    return i0, i1, compute(shard, win, method, k, r)

@@ -1,0 +1,226 @@
+"""Device-side entry points: torch tensors as buffers, work done by libdocthresh_b200.
+
+Every function here launches a kernel from libdocthresh_b200.so through the
+C ABI (include/docthresh_b200.h) on the current torch CUDA stream.  Inputs
+may be host numpy arrays (copied to the device) or CUDA uint8 tensors (used in
+place).  There is no CPU path: without a CUDA device these raise.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+METHOD_CODES = {"sauvola": _lib.DTB_METHOD_SAUVOLA, "niblack": _lib.DTB_METHOD_NIBLACK}
+
+_torch = None
+
+
+def torch_mod():
+    global _torch
+    if _torch is None:
+        import torch
+        _torch = torch
+    if not _torch.cuda.is_available():
+        raise RuntimeError("paper_1210_3165_b200 needs a CUDA device (there is no CPU fallback)")
+    return _torch
+
+
+def is_device_tensor(x) -> bool:
+    if _torch is None and type(x).__module__.split(".")[0] != "torch":
+        return False
+    import torch
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def is_host_tensor(x) -> bool:
+    if _torch is None and type(x).__module__.split(".")[0] != "torch":
+        return False
+    import torch
+    return isinstance(x, torch.Tensor) and not x.is_cuda
+
+
+def _stream(stream=None) -> int:
+    torch = torch_mod()
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _check_device_image(t, ndim: int, what: str):
+    torch = torch_mod()
+    if t.dtype != torch.uint8:
+        raise ValueError(f"{what}: expected a uint8 CUDA tensor, got {t.dtype}")
+    if t.dim() != ndim:
+        raise ValueError(f"expected a {ndim}-D image, got shape {tuple(t.shape)}")
+    if t.numel() == 0:
+        raise ValueError("image is empty")
+    if t.stride(-1) != 1 or (ndim == 3 and t.stride(1) != 3):
+        t = t.contiguous()
+    return t
+
+
+def to_device(arr, ndim: int = 2, what: str = "image"):
+    """Host numpy (already validated) or CUDA tensor -> CUDA uint8 tensor with unit inner stride."""
+    torch = torch_mod()
+    if is_device_tensor(arr):
+        return _check_device_image(arr, ndim, what)
+    if is_host_tensor(arr):
+        return arr.contiguous().to("cuda", non_blocking=True)
+    a = np.ascontiguousarray(arr, dtype=np.uint8)
+    return torch.from_numpy(a).to("cuda")
+
+
+def binarize(gray, win: int, method: str, k: float, r: float, want_tmap: bool = True,
+             stream=None):
+    """Whole-image binarize -> (binary uint8 tensor, tmap float64 tensor or None)."""
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
+    tmap = torch.empty((h, w), dtype=torch.float64, device=g.device) if want_tmap else None
+    rc = _lib.lib().dtb_binarize(
+        g.data_ptr(), g.stride(0), h, w, 0, h, 0, h, out.data_ptr(), out.stride(0),
+        tmap.data_ptr() if tmap is not None else None, (tmap.stride(0) * 8) if tmap is not None else 0,
+        int(win), METHOD_CODES[method], float(k), float(r), _stream(stream))
+    _lib.check(rc, "dtb_binarize")
+    return out, tmap
+
+
+def binarize_band(buf, row0_global: int, rows_global: int, out_begin: int, out_end: int,
+                  win: int, method: str, k: float, r: float, out=None, stream=None):
+    """Binarize global rows [out_begin, out_end) from a buffer holding rows [row0, row0+len)."""
+    torch = torch_mod()
+    g = to_device(buf)
+    in_rows, w = g.shape
+    if out is None:
+        out = torch.empty((out_end - out_begin, w), dtype=torch.uint8, device=g.device)
+    rc = _lib.lib().dtb_binarize(
+        g.data_ptr(), g.stride(0), in_rows, w, int(row0_global), int(rows_global), int(out_begin),
+        int(out_end), out.data_ptr(), out.stride(0), None, 0, int(win), METHOD_CODES[method],
+        float(k), float(r), _stream(stream))
+    _lib.check(rc, "dtb_binarize")
+    return out
+
+
+def binarize_batch(stack, win: int, method: str, k: float, r: float, out=None, stream=None):
+    """(N, H, W) uint8 CUDA stack -> (N, H, W) binary, one launch."""
+    torch = torch_mod()
+    s = stack if is_device_tensor(stack) else torch.from_numpy(np.ascontiguousarray(stack)).to("cuda")
+    s = s.contiguous()
+    n, h, w = s.shape
+    if out is None:
+        out = torch.empty_like(s)
+    rc = _lib.lib().dtb_binarize_batch(
+        s.data_ptr(), s.stride(0), n, h, w, out.data_ptr(), out.stride(0), int(win),
+        METHOD_CODES[method], float(k), float(r), _stream(stream))
+    _lib.check(rc, "dtb_binarize_batch")
+    return out
+
+
+def window_stats(gray, win: int, want=("mean", "std", "count"), stream=None):
+    """dict of requested (rows, cols) device tensors among S, Q, count, mean, std."""
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    dt = {"S": torch.int64, "Q": torch.int64, "count": torch.int32, "mean": torch.float64,
+          "std": torch.float64}
+    outs = {k: torch.empty((h, w), dtype=dt[k], device=g.device) for k in want}
+    ptr = lambda k: outs[k].data_ptr() if k in outs else None  # noqa: E731
+    rc = _lib.lib().dtb_window_stats(g.data_ptr(), g.stride(0), h, w, int(win), ptr("S"),
+                                     ptr("Q"), ptr("count"), ptr("mean"), ptr("std"),
+                                     _stream(stream))
+    _lib.check(rc, "dtb_window_stats")
+    return outs
+
+
+def sampled(gray, offsets, method: str | None = None, k: float = 0.0, r: float = 128.0,
+            want_tmap: bool = True, stream=None):
+    """Mask-restricted statistics (stats.py:133-163) or binarization with them.
+
+    method None -> dict(mean, std, count); else (binary, tmap or None).
+    """
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int32).reshape(-1, 2))
+    dev_offs = torch.from_numpy(offs).to("cuda")
+    L = _lib.lib()
+    if method is None:
+        mean = torch.empty((h, w), dtype=torch.float64, device=g.device)
+        std = torch.empty_like(mean)
+        cnt = torch.empty((h, w), dtype=torch.int32, device=g.device)
+        rc = L.dtb_sampled_stats(g.data_ptr(), g.stride(0), h, w, dev_offs.data_ptr(),
+                                 len(offs), mean.data_ptr(), std.data_ptr(), cnt.data_ptr(),
+                                 None, 0, 0, 0.0, 1.0, _stream(stream))
+        _lib.check(rc, "dtb_sampled_stats")
+        return {"mean": mean, "std": std, "count": cnt}
+    out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
+    tmap = torch.empty((h, w), dtype=torch.float64, device=g.device) if want_tmap else None
+    rc = L.dtb_sampled_stats(g.data_ptr(), g.stride(0), h, w, dev_offs.data_ptr(), len(offs),
+                             None, None, None, out.data_ptr(),
+                             tmap.data_ptr() if tmap is not None else None,
+                             METHOD_CODES[method], float(k), float(r), _stream(stream))
+    _lib.check(rc, "dtb_sampled_stats")
+    return out, tmap
+
+
+def to_gray(rgb, stream=None):
+    torch = torch_mod()
+    t = to_device(rgb, ndim=3, what="rgb")
+    h, w, _ = t.shape
+    out = torch.empty((h, w), dtype=torch.uint8, device=t.device)
+    rc = _lib.lib().dtb_to_gray(t.data_ptr(), t.stride(0), out.data_ptr(), out.stride(0), h, w,
+                                _stream(stream))
+    _lib.check(rc, "dtb_to_gray")
+    return out
+
+
+def rgb_binarize(rgb, win: int, method: str, k: float, r: float, want_gray: bool = False,
+                 stream=None):
+    torch = torch_mod()
+    t = to_device(rgb, ndim=3, what="rgb")
+    h, w, _ = t.shape
+    out = torch.empty((h, w), dtype=torch.uint8, device=t.device)
+    gray = torch.empty((h, w), dtype=torch.uint8, device=t.device)
+    rc = _lib.lib().dtb_rgb_binarize(t.data_ptr(), t.stride(0), h, w, out.data_ptr(),
+                                     out.stride(0), gray.data_ptr(), gray.stride(0), int(win),
+                                     METHOD_CODES[method], float(k), float(r), _stream(stream))
+    _lib.check(rc, "dtb_rgb_binarize")
+    return (out, gray) if want_gray else out
+
+
+def histogram(gray, stream=None):
+    """256-bin histogram (uint64) of a gray image, on the device."""
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    hist = torch.zeros(256, dtype=torch.int64, device=g.device)
+    rc = _lib.lib().dtb_histogram(g.data_ptr(), g.stride(0), h, w, hist.data_ptr(),
+                                  _stream(stream))
+    _lib.check(rc, "dtb_histogram")
+    return hist
+
+
+def apply_global(gray, t: int, stream=None):
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
+    rc = _lib.lib().dtb_apply_global(g.data_ptr(), g.stride(0), h, w, int(t), out.data_ptr(),
+                                     out.stride(0), _stream(stream))
+    _lib.check(rc, "dtb_apply_global")
+    return out
+
+
+def integral_tables(gray, stream=None):
+    """(H+1, W+1) int64 summed-area tables of f and f^2 (stats.py:82-91)."""
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    s = torch.empty((h + 1, w + 1), dtype=torch.int64, device=g.device)
+    sq = torch.empty_like(s)
+    rc = _lib.lib().dtb_integral_tables(g.data_ptr(), g.stride(0), h, w, s.data_ptr(),
+                                        sq.data_ptr(), _stream(stream))
+    _lib.check(rc, "dtb_integral_tables")
+    return s, sq
