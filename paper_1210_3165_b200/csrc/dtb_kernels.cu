@@ -19,12 +19,14 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
 
 #include "docthresh_b200.h"
 #include "dtb_common.cuh"
+#include "dtb_slide.cuh"
 
 namespace dtb {
 
@@ -365,6 +367,18 @@ static int launch_strip(StripParams p, int n_images, cudaStream_t st) {
     return e == cudaSuccess ? DTB_OK : cuda_fail(e, "strip_kernel launch");
 }
 
+// The fast kernel keeps 32-bit sums: every window sum must stay < 2^32, and the strip
+// (<= 8 warps = 8192 columns) must hold a window plus 32 outputs.
+static bool slide_ok(int r, int cols, int rows, const void* base, int64_t pitch,
+                     int64_t stride) {
+    if (const char* env = getenv("DTB_FORCE_V1")) { if (env[0] == '1') return false; }
+    // rows are staged with 16-byte bulk copies
+    if (((uintptr_t)base | (uintptr_t)pitch | (uintptr_t)stride) & 15) return false;
+    const double rx = std::min(r, cols - 1), ry = std::min(r, rows - 1);
+    const double nmax = (2.0 * rx + 1.0) * (2.0 * ry + 1.0);
+    return 65025.0 * nmax < 4294967296.0 && 2 * rx + 16 + 32 <= 8192;
+}
+
 static int check_window(int win) {
     if (win < 3 || (win % 2) == 0)
         return fail(DTB_E_INVALID, "window: must be an odd integer >= 3, got %d", win);
@@ -425,6 +439,16 @@ int dtb_binarize(const uint8_t* gray, int64_t pitch, int32_t in_rows, int32_t co
         return fail(DTB_E_INVALID,
                     "rows: band needs global rows [%d,%d) but buffer holds [%d,%d)", need0,
                     need1, row0_global, row0_global + in_rows);
+    if (!tmap && slide_ok(rad, cols, rows_global, gray, pitch, 0)) {
+        SlideParams q{};
+        q.in = gray; q.pitch = pitch; q.cols = cols; q.row0 = row0_global; q.H = rows_global;
+        q.out_begin = out_row_begin; q.out_end = out_row_end; q.r = rad;
+        q.rx = std::min(rad, cols - 1);
+        q.bin = binary; q.bin_pitch = binary_pitch; q.method = method; q.k = k; q.rr = r;
+        if (out_row_end <= out_row_begin) return DTB_OK;
+        const cudaError_t e = launch_slide(q, 1, num_sms(), (cudaStream_t)stream);
+        return e == cudaSuccess ? DTB_OK : cuda_fail(e, "slide_kernel launch");
+    }
     StripParams p{};
     p.in = gray; p.pitch = pitch; p.cols = cols; p.row0 = row0_global; p.H = rows_global;
     p.out_begin = out_row_begin; p.out_end = out_row_end; p.r = rad;
@@ -443,6 +467,17 @@ int dtb_binarize_batch(const uint8_t* gray, int64_t image_stride, int32_t n_imag
     if (rows <= 0 || cols <= 0) return fail(DTB_E_INVALID, "image is empty");
     if (n_images < 0) return fail(DTB_E_INVALID, "n_images: negative");
     if (n_images > 65535) return fail(DTB_E_UNSUPPORTED, "n_images: at most 65535 per call");
+    if (slide_ok(win / 2, cols, rows, gray, cols, image_stride)) {
+        SlideParams q{};
+        q.in = gray; q.pitch = cols; q.img_stride = image_stride; q.cols = cols; q.row0 = 0;
+        q.H = rows; q.out_begin = 0; q.out_end = rows; q.r = win / 2;
+        q.rx = std::min(win / 2, cols - 1);
+        q.bin = binary; q.bin_pitch = cols; q.out_stride = out_stride;
+        q.method = method; q.k = k; q.rr = r;
+        if (n_images == 0) return DTB_OK;
+        const cudaError_t e = launch_slide(q, n_images, num_sms(), (cudaStream_t)stream);
+        return e == cudaSuccess ? DTB_OK : cuda_fail(e, "slide_kernel launch");
+    }
     StripParams p{};
     p.in = gray; p.pitch = cols; p.img_stride = image_stride; p.cols = cols; p.row0 = 0;
     p.H = rows; p.out_begin = 0; p.out_end = rows; p.r = win / 2;

@@ -1,0 +1,640 @@
+// dtb_slide.cu -- the fast fused sliding-sum binarization kernel (K2) for sm_100a.
+//
+// Replaces, for the binary output, threshold.py:121-148 -> stats.py:166-191 ->
+// stats.py:50-54 -> threshold.py:143-147 of the reference, bit for bit.
+//
+// Layout.  One CTA owns a vertical strip and a band of output rows.  Strip s produces output
+// columns [X0, X0+TW), X0 = s*TW (TW = 0 mod 32).  Its column index space i <-> image column
+// xc0 + i with xc0 = X0 - rx - alpha = 0 mod 16 (alpha = (-rx) mod 16), i in [0, NC),
+// NC = V*NT (V = 16 or 32 columns per thread).  Thread t owns columns [Vt, Vt+V): it keeps
+// their exact running column sums
+//   cS[j] = sum f, cQ[j] = sum f^2   over rows [y-r, y+r] (clipped)
+// in registers and slides them down the band (+ row y+r, - row y-r-1, 2 LDG.128 each).
+// Per output row the CTA forms the inclusive horizontal prefix P of the column sums in shared
+// memory (uint32, exact mod 2^32 -- every true window sum is < 2^32 for W <= 255): per-thread
+// totals -> warp shuffle scan -> cross-warp totals -> per-thread running prefix, stored as
+// logical word k = P[k-1] (so each thread writes 8 aligned 16-byte chunks).  Shared memory is
+// padded one 16-byte chunk per 8 (chunk L lives at L + L/8), which makes both the per-thread
+// stores and the run loads bank-conflict free.  Output x = X0 + Vt + j has window indices
+// [alpha+Vt+j, alpha+2rx+Vt+j]:  S = P[alpha+2rx+Vt+j] - P[alpha-1+Vt+j];
+// the two runs are misaligned by (-rx) mod 4 and (rx+1) mod 4 words, resolved at compile time
+// (RXM4 template) so both are read with LDS.128.
+//
+// Decision.  The threshold is formed in fp32 from the EXACT integer D = n*Q - S^2 (>= 0, no
+// cancellation; n = N = W^2 for unclipped windows, n = ny*nx at image borders):
+//   Sauvola  t = S * ((1-k)/n + k/(R n^2) * sqrt(D))        Niblack  t = S/n + k/n * sqrt(D)
+// The host bounds |t_fp32 - t_reference| (fp32 error of this sequence + the reference's own
+// fp64 rounding of var/std) by `tol`.  A pixel with |f - t_fp32| >= tol is decided by the sign;
+// if any of a thread's 32 pixels is within tol (~1e-5 of pixels), the thread replays the
+// reference fp64 sequence for those pixels (out of line, rare).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "docthresh_b200.h"
+#include "dtb_common.cuh"
+#include "dtb_slide.cuh"
+
+namespace dtb {
+
+// Guarded byte-wise load of 4 words (image edges / unaligned buffers); out of line.
+__device__ __noinline__ uint4 ldg16_slow(const uint8_t* rowp, int c0, int cols) {
+    uint32_t w[4];
+    for (int q = 0; q < 4; ++q) {
+        uint32_t v = 0;
+        for (int b = 0; b < 4; ++b) {
+            const int c = c0 + 4 * q + b;
+            if (c >= 0 && c < cols) v |= (uint32_t)__ldg(rowp + c) << (8 * b);
+        }
+        w[q] = v;
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ uint4 ldg16(const uint8_t* rowp, int c0, int cols, bool vec) {
+    // 16 bytes of one image row at columns [c0, c0+16), zeros outside [0, cols); c0 = 0 mod 16.
+    if (c0 >= 0 && c0 + 16 <= cols) {
+        if (vec) return __ldg(reinterpret_cast<const uint4*>(rowp + c0));
+    } else if (c0 + 16 <= 0 || c0 >= cols) {
+        return make_uint4(0, 0, 0, 0);
+    }
+    return ldg16_slow(rowp, c0, cols);
+}
+
+__device__ __forceinline__ void ldg32B(const uint8_t* rowp, int c0, int cols, bool vec,
+                                       uint32_t (&w)[8]) {
+    const uint4 a = ldg16(rowp, c0, cols, vec);
+    const uint4 b = ldg16(rowp, c0 + 16, cols, vec);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+}
+
+template <int NW>
+__device__ __forceinline__ uint32_t byte_at(const uint32_t (&w)[NW], int j) {
+    return __byte_perm(w[j >> 2], 0u, 0x4440 | (j & 3));
+}
+
+// prmt.b32 with the raw selector (sign-replicate mode available: nibble bit 3 set copies the
+// sign bit of the selected byte into all 8 bits; __byte_perm masks selectors to 3 bits).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+// padded shared-memory position (in words) of logical chunk L
+__device__ __forceinline__ int pchunk_word(int L) { return 4 * (L + (L >> 3)); }
+
+__device__ __forceinline__ float sqrt_ftz(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// f - t_fp32 for one pixel.  cA/cC: per-launch constants for n = N (interior); at borders
+// (BORDER) they are rebuilt from the pixel's own count n with an fp32 reciprocal.
+template <int METHOD, bool BORDER>
+__device__ __forceinline__ float fast_diff(uint32_t S, uint32_t Q, uint32_t f, uint32_t n,
+                                           float cA, float cC, float a, float c) {
+    const uint64_t D = (uint64_t)n * Q - (uint64_t)S * S;  // exact, >= 0
+    const float sD = sqrt_ftz((float)D);
+    const float Sf = (float)S;
+    if (BORDER) {
+        const float rn = rcp_ftz((float)n);
+        if (METHOD == DTB_METHOD_SAUVOLA) {
+            cA = a * rn;           // (1-k)/n
+            cC = c * (rn * rn);    // k/(R n^2)
+        } else {
+            cA = rn;               // 1/n
+            cC = c * rn;           // k/n
+        }
+    }
+    if (METHOD == DTB_METHOD_SAUVOLA) return __fmaf_rn(-Sf, __fmaf_rn(sD, cC, cA), (float)f);
+    return __fmaf_rn(-cC, sD, __fmaf_rn(-cA, Sf, (float)f));
+}
+
+// Reference fp64 decision for one pixel (threshold.py:143-147 over stats.py:50-54).
+__device__ __noinline__ uint32_t exact_white(uint32_t S, uint32_t Q, double n, uint32_t f,
+                                             int method, double k, double rr) {
+    double mean, sd;
+    finish_exact((double)S, (double)Q, n, mean, sd);
+    const double t = threshold_exact(mean, sd, method, k, rr);
+    return ((double)f < t) ? 0u : 0xFFu;
+}
+
+// Rare path, out of line: re-decide this thread's 32 pixels, the uncertain ones (|f - t32| < tol)
+// with the reference fp64 sequence.  S/Q are read back from the shared prefix (valid until the next
+// row's first barrier); corrected bytes are written after the vector stores (program order).
+template <int METHOD>
+__device__ __noinline__ void fix_uncertain(const uint32_t* sPS, const uint32_t* sPQ, int a_word,
+                                           int b_word, const uint8_t* frow, uint8_t* orow,
+                                           int xo, int nv, int cols, int ny, int r, uint32_t N,
+                                           float cA, float cC, float a, float c, float tol,
+                                           double k, double rr) {
+    for (int j = 0; j < nv; ++j) {
+        const int x = xo + j;
+        if (x < 0 || x >= cols) continue;
+        const int la = a_word + j, lb = b_word + j;  // logical words
+        const int pa = pchunk_word(la >> 2) + (la & 3), pb = pchunk_word(lb >> 2) + (lb & 3);
+        const uint32_t S = sPS[pb] - sPS[pa];
+        const uint32_t Q = sPQ[pb] - sPQ[pa];
+        const uint32_t f = frow[x];
+        const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
+        const uint32_t n = (uint32_t)(ny * nx);
+        const float d = (n == N) ? fast_diff<METHOD, false>(S, Q, f, n, cA, cC, a, c)
+                                 : fast_diff<METHOD, true>(S, Q, f, n, cA, cC, a, c);
+        // rewrite every pixel of the thread: the caller's decision may have used the other
+        // (border) constant set, so its certified set can differ from this one's
+        orow[x] = (fabsf(d) >= tol) ? (d < 0.f ? 0 : 255)
+                                    : (uint8_t)exact_white(S, Q, (double)n, f, METHOD, k, rr);
+    }
+}
+
+// One row of 32 outputs for this thread: S/Q from the shared prefix, f from global (row y),
+// fp32 certified decision, 8-byte stores.  Returns whether any pixel was uncertain.
+// aw/bw: shared-memory word addresses of the 9 chunks of the A and B runs (precomputed).
+template <int V, int RXM4, int METHOD, bool BORDER>
+__device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t* sPQ,
+                                            const int (&aw)[V / 4 + 1], const int (&bw)[V / 4 + 1],
+                                            const uint8_t* fsm, uint8_t* orow, int xo,
+                                            int cols, bool full, int ny, int r,
+                                            const SlideParams& p) {
+    constexpr int MA = (4 - RXM4) & 3;  // misalignment (words) of the A run
+    constexpr int MB = (RXM4 + 1) & 3;  // misalignment (words) of the B run
+    uint32_t fw[V / 4];  // row y pixel values of this thread's V outputs, from the shared stage
+#pragma unroll
+    for (int q = 0; q < V / 16; ++q) {
+        const uint4 v = *reinterpret_cast<const uint4*>(fsm + 16 * q);
+        fw[4 * q] = v.x; fw[4 * q + 1] = v.y; fw[4 * q + 2] = v.z; fw[4 * q + 3] = v.w;
+    }
+    float mind = 3.0e38f;
+    uint32_t ow[V / 4];
+#pragma unroll
+    for (int g = 0; g < V / 8; ++g) {  // groups of 8 outputs
+        uint32_t S8[8], Q8[8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t* sp = h ? sPQ : sPS;
+            uint32_t A[12], B[12];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (q < 2 || MA) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(sp + aw[2 * g + q]);
+                    A[4 * q] = v.x; A[4 * q + 1] = v.y; A[4 * q + 2] = v.z; A[4 * q + 3] = v.w;
+                }
+                if (q < 2 || MB) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(sp + bw[2 * g + q]);
+                    B[4 * q] = v.x; B[4 * q + 1] = v.y; B[4 * q + 2] = v.z; B[4 * q + 3] = v.w;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t v = B[MB + j] - A[MA + j];
+                if (h) Q8[j] = v; else S8[j] = v;
+            }
+        }
+        const uint32_t fa = fw[2 * g], fb = fw[2 * g + 1];
+        float d[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t f = __byte_perm(j < 4 ? fa : fb, 0u, 0x4440 | (j & 3));
+            uint32_t n = p.N;
+            if (BORDER) {
+                const int x = xo + 8 * g + j;
+                n = (uint32_t)(ny * (min(x + r, cols - 1) - max(x - r, 0) + 1));
+            }
+            d[j] = fast_diff<METHOD, BORDER>(S8[j], Q8[j], f, n, p.cA, p.cC, p.a, p.c);
+            mind = fminf(mind, fabsf(d[j]));
+        }
+        // byte = 0x00 if f < t (diff negative) else 0xFF: sign-replicate the diff's top byte
+        ow[2 * g] = ~prmt(prmt(__float_as_uint(d[0]), __float_as_uint(d[1]), 0xFBFB),
+                          prmt(__float_as_uint(d[2]), __float_as_uint(d[3]), 0xFBFB), 0x5410);
+        ow[2 * g + 1] = ~prmt(prmt(__float_as_uint(d[4]), __float_as_uint(d[5]), 0xFBFB),
+                              prmt(__float_as_uint(d[6]), __float_as_uint(d[7]), 0xFBFB), 0x5410);
+    }
+    if (full) {
+#pragma unroll
+        for (int q = 0; q < V / 16; ++q)
+            *reinterpret_cast<uint4*>(orow + xo + 16 * q) =
+                make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int x = xo + j;
+            if (x >= 0 && x < cols) orow[x] = (uint8_t)(ow[j >> 2] >> (8 * (j & 3)));
+        }
+    }
+    return mind < p.tol;
+}
+
+// ---- asynchronous row staging: cp.async.bulk (TMA engine, no tensor map) + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// Sequence of pipeline items for one CTA: warm-up rows g0..g1 (entering row only), then
+// main row steps y = ya..yb-1 (entering row y+r, leaving row y-r-1, centre row y).
+struct Items {
+    int g0, nwarm, ya, n;
+};
+
+// register budget: V=16 fits 128 registers without spills (4 CTAs x 4 warps per SM)
+#ifndef DTB_SLIDE_MINB
+#define DTB_SLIDE_MINB(V) ((V) == 16 ? 2 : 1)
+#endif
+
+template <int V, int RXM4, int METHOD>
+__global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlideParams p) {
+    constexpr int MA = (4 - RXM4) & 3;
+    constexpr int MB = (RXM4 + 1) & 3;
+    constexpr int NS = SLIDE_STAGES;
+    extern __shared__ __align__(128) uint32_t sm[];
+    const int NCp = slide_padded_words(p.NC);
+    uint32_t* sPS = sm;
+    uint32_t* sPQ = sm + NCp;
+    uint32_t* sWS = sm + 2 * NCp;  // per-warp totals (8 + 8 words)
+    uint32_t* sWQ = sWS + 8;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sWS + 16);   // NS barriers
+    uint64_t* empty = full + NS;                              // NS barriers
+    uint8_t* ring = reinterpret_cast<uint8_t*>(empty + NS);   // NS stages x (E, O, F) x NC
+    const int nwarps = (blockDim.x + 31) >> 5;
+
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint8_t* in = p.in + (int64_t)blockIdx.z * p.img_stride;
+    const int X0 = (int)blockIdx.x * p.TW;
+    const int alpha = (16 - (p.rx & 15)) & 15;
+    const int xc0 = X0 - p.rx - alpha;
+    const int ya = p.out_begin + (int)blockIdx.y * p.TH;
+    const int yb = min(ya + p.TH, p.out_end);
+    if (ya >= yb) return;
+    const uint8_t* in0 = in - (int64_t)p.row0 * p.pitch;  // row g at in0 + g*pitch
+    // bulk-copied column range of the strip, [c_lo, c_hi16) (16-byte multiples), + byte tail
+    const int c_lo = max(xc0, 0);
+    const int c_hi = min(xc0 + p.NC, p.cols);
+    const int c_hi16 = c_lo + ((max(c_hi - c_lo, 0)) & ~15);
+    const int f_hi = min(X0 + p.TW, p.cols);
+    const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
+
+    Items it;
+    it.g0 = max(ya - p.r, 0);
+    it.nwarm = min(ya + p.r, p.H - 1) - it.g0 + 1;
+    it.ya = ya;
+    it.n = it.nwarm + (yb - ya);
+
+    // ---- init: zero the ring (columns outside the image stay zero), barriers
+    {
+        uint4* r4 = reinterpret_cast<uint4*>(ring);
+        const int n16 = NS * 3 * p.NC / 16;
+        for (int i = t; i < n16; i += blockDim.x) r4[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], nwarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // producer (thread 0): stage item k.  Rows outside the image are not copied; consumers
+    // treat them as zero.  The byte tail beyond the last 16-byte chunk is written by thread 0
+    // with generic stores (visible to consumers after the barriers in between).
+    auto issue = [&](int k) {
+        const int s = k % NS;
+        if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
+        uint8_t* E = ring + (size_t)s * 3 * p.NC;
+        uint8_t* O = E + p.NC;
+        uint8_t* F = O + p.NC;
+        int ge, go = -1, gf = -1;
+        if (k < it.nwarm) {
+            ge = it.g0 + k;
+        } else {
+            const int y = it.ya + (k - it.nwarm);
+            gf = y;
+            ge = (k == it.nwarm) ? -1 : y + p.r;
+            go = (k == it.nwarm) ? -1 : y - p.r - 1;
+            if (ge >= p.H) ge = -1;
+        }
+        uint32_t bytes = 0;
+        const uint32_t rowb = (uint32_t)(c_hi16 - c_lo), fb = (uint32_t)(f_hi16 - X0);
+        if (ge >= 0) bytes += rowb;
+        if (go >= 0) bytes += rowb;
+        if (gf >= 0) bytes += fb;
+        mbar_expect_tx(&full[s], bytes);
+        if (ge >= 0 && rowb) bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s]);
+        if (go >= 0 && rowb) bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s]);
+        if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s]);
+        for (int c = c_hi16; c < c_hi; ++c) {
+            if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
+            if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+        }
+        for (int c = f_hi16; c < f_hi; ++c)
+            if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+    };
+    // lookahead of NS-1 items: item k+NS-1 reuses the stage of item k-1, which every warp has
+    // released by the time thread 0 passes the first barrier of step k (main steps) -- so the
+    // producer never waits on the slowest warp while holding the barrier up.
+    if (t == 0)
+        for (int k = 0; k < min(NS - 1, it.n); ++k) issue(k);
+
+    uint32_t cS[V], cQ[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) { cS[j] = 0; cQ[j] = 0; }
+    uint32_t TS = 0, TQ = 0;  // thread totals sum_j cS[j], sum_j cQ[j], kept incrementally
+
+    const int xo = X0 + V * t;  // this thread's V output columns
+    const bool has_out = (V * t + V + 2 * p.rx + alpha <= p.NC) && (V * t < p.TW) &&
+                         (xo < p.cols);
+    const bool out_full = has_out && (xo + 32 <= p.cols) &&
+                          ((reinterpret_cast<uintptr_t>(p.bin) | (uintptr_t)p.bin_pitch |
+                            (uintptr_t)p.out_stride) & 15) == 0;
+    const bool x_interior = (p.rx == p.r) && (xo - p.r >= 0) && (xo + V - 1 + p.r <= p.cols - 1);
+    const int la0 = (alpha + V * t - MA) >> 2;
+    const int lb0 = (alpha + 2 * p.rx + 1 + V * t - MB) >> 2;
+    int aw[V / 4 + 1], bw[V / 4 + 1];
+#pragma unroll
+    for (int i = 0; i < V / 4 + 1; ++i) { aw[i] = pchunk_word(la0 + i); bw[i] = pchunk_word(lb0 + i); }
+    // a warp with any x-border thread runs the (per-pixel count) border variant uniformly
+    const bool x_border_warp = __any_sync(__activemask(), has_out && !x_interior);
+    uint8_t* obase = p.bin + (int64_t)blockIdx.z * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
+
+    auto release = [&](int k) {  // this warp is done with item k's stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[k % NS]);
+    };
+
+    // ---- warm-up: vertical window of the first output row
+    for (int k = 0; k < it.nwarm; ++k) {
+        const int s = k % NS;
+        mbar_wait(&full[s], (k / NS) & 1);
+        const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + V * t);
+        uint32_t w[V / 4];
+#pragma unroll
+        for (int q = 0; q < V / 16; ++q) {
+            const uint4 a = E[q];
+            w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const uint32_t v = byte_at(w, j);
+            cS[j] += v;
+            cQ[j] += v * v;
+        }
+        release(k);
+        if (t == 0 && k + NS - 1 < it.n) issue(k + NS - 1);
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) { TS += cS[j]; TQ += cQ[j]; }
+
+    for (int k = it.nwarm; k < it.n; ++k) {
+        const int y = it.ya + (k - it.nwarm);
+        const int s = k % NS;
+        mbar_wait(&full[s], (k / NS) & 1);
+        const uint8_t* stage = ring + (size_t)s * 3 * p.NC;
+        if (k > it.nwarm) {
+            const bool ein = y + p.r < p.H, oin = y - p.r - 1 >= 0;
+            uint32_t e[V / 4], o[V / 4];
+            {
+                const uint4* E = reinterpret_cast<const uint4*>(stage + V * t);
+                const uint4* O = reinterpret_cast<const uint4*>(stage + p.NC + V * t);
+#pragma unroll
+                for (int q = 0; q < V / 16; ++q) {
+                    const uint4 a = ein ? E[q] : make_uint4(0, 0, 0, 0);
+                    const uint4 b = oin ? O[q] : make_uint4(0, 0, 0, 0);
+                    e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
+                    o[4 * q] = b.x; o[4 * q + 1] = b.y; o[4 * q + 2] = b.z; o[4 * q + 3] = b.w;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
+                const uint32_t dv = ev - ov;
+                cS[j] += dv;
+                cQ[j] += dv * (ev + ov);
+            }
+#pragma unroll
+            for (int q = 0; q < V / 4; ++q) {  // 4 columns per dp4a: sum of bytes / of squares
+                TS += (uint32_t)__dp4a(e[q], 0x01010101u, 0u) - (uint32_t)__dp4a(o[q], 0x01010101u, 0u);
+                TQ += (uint32_t)__dp4a(e[q], e[q], 0u) - (uint32_t)__dp4a(o[q], o[q], 0u);
+            }
+        }
+
+        // ---- horizontal inclusive prefix, exact mod 2^32 (lanes >= the warp's live count
+        // never exist: blockDim is a multiple of 32)
+        uint32_t iS = TS, iQ = TQ;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
+            const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
+            if (lane >= off) { iS += vs; iQ += vq; }
+        }
+        if (lane == 31) { sWS[warp] = iS; sWQ[warp] = iQ; }
+        __syncthreads();
+        if (t == 0 && k + NS - 1 < it.n) issue(k + NS - 1);
+        uint32_t bS = iS - TS, bQ = iQ - TQ;
+        for (int w = 0; w < warp; ++w) { bS += sWS[w]; bQ += sWQ[w]; }
+        // logical word Vt + m holds P[Vt + m - 1]: the first slot is this thread's base
+#pragma unroll
+        for (int j = 0; j < V; j += 4) {
+            uint4 vs, vq;
+            vs.x = bS; vq.x = bQ;
+            bS += cS[j]; bQ += cQ[j];
+            vs.y = bS; vq.y = bQ;
+            bS += cS[j + 1]; bQ += cQ[j + 1];
+            vs.z = bS; vq.z = bQ;
+            bS += cS[j + 2]; bQ += cQ[j + 2];
+            vs.w = bS; vq.w = bQ;
+            bS += cS[j + 3]; bQ += cQ[j + 3];
+            const int pw = pchunk_word((V / 4) * t + j / 4);
+            *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
+            *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
+        }
+        if (t == blockDim.x - 1) {  // logical word NC = P[NC - 1]
+            const int pw = pchunk_word(p.NC / 4);
+            sPS[pw] = bS;
+            sPQ[pw] = bQ;
+        }
+        __syncthreads();
+
+        // ---- outputs
+        if (has_out) {
+            const bool y_interior = (y - p.r >= 0) && (y + p.r <= p.H - 1);
+            uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
+            const int ny = min(y + p.r, p.H - 1) - max(y - p.r, 0) + 1;
+            const uint8_t* fsm = stage + 2 * p.NC + V * t;
+            bool unc;
+            if (y_interior && !x_border_warp)
+                unc = row_outputs<V, RXM4, METHOD, false>(sPS, sPQ, aw, bw, fsm, orow, xo, p.cols,
+                                                       out_full, ny, p.r, p);
+            else
+                unc = row_outputs<V, RXM4, METHOD, true>(sPS, sPQ, aw, bw, fsm, orow, xo, p.cols,
+                                                      out_full, ny, p.r, p);
+            if (__builtin_expect(unc, 0))
+                fix_uncertain<METHOD>(sPS, sPQ, alpha + V * t, alpha + 2 * p.rx + 1 + V * t,
+                                      in0 + (int64_t)y * p.pitch, orow, xo, V, p.cols, ny, p.r, p.N,
+                                      p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
+        }
+        release(k);
+    }
+}
+
+// Certified tolerance (see header comment):  |t_fp32 - t_exact| <= E_fast and
+// |t_reference - t_exact| <= E_ref, so |f - t_fp32| >= tol = 2 (E_fast + E_ref) fixes the sign of
+// f - t_reference.  E_ref: the reference's var = Q/n - mean^2 carries <= 5u Q/n <= 3.6e-11
+// absolute error (u = 2^-53, Q/n <= 255^2), hence std carries <= sqrt(3.6e-11) = 6.0e-6;
+// Sauvola multiplies it by mean*k/R <= 255 k/R, Niblack by |k|.  E_fast: D is exact; the fp32
+// rounding of D, sqrt.approx / rcp.approx (<= 2^-21 assumed each), the rounded constants and
+// the fmas give a relative error <= 1.1e-6 on the threshold; we use 1.5e-6 times a bound on |t|.
+void slide_constants(SlideParams& p) {
+    const double W = 2.0 * p.r + 1.0, N = W * W;
+    p.N = (uint32_t)N;
+    const double sd_err = 6.6e-6, rel = 1.5e-6;
+    double e_ref, e_fast;
+    if (p.method == DTB_METHOD_SAUVOLA) {
+        const double kr = p.k / p.rr;
+        p.a = (float)(1.0 - p.k);
+        p.c = (float)kr;
+        p.cA = (float)((1.0 - p.k) / N);
+        p.cC = (float)(kr / (N * N));
+        e_ref = 255.0 * kr * sd_err;
+        e_fast = 255.0 * (1.0 + std::fabs(p.k) * (127.5 / p.rr + 1.0)) * rel;
+    } else {
+        p.a = 1.0f;
+        p.c = (float)p.k;
+        p.cA = (float)(1.0 / N);
+        p.cC = (float)(p.k / N);
+        e_ref = std::fabs(p.k) * sd_err;
+        e_fast = (255.0 + std::fabs(p.k) * 127.5) * rel;
+    }
+    p.tol = (float)(2.0 * (e_ref + e_fast) + 1e-6);
+}
+
+template <int V, int RXM4, int METHOD>
+static cudaError_t run_slide(dim3 grid, int nt, size_t smem, const SlideParams& p,
+                             cudaStream_t st) {
+    auto kern = slide_kernel<V, RXM4, METHOD>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, nt, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int V, int RXM4, int METHOD>
+static int occupancy(int nt, size_t smem) {
+    int blocks = 0;
+    auto kern = slide_kernel<V, RXM4, METHOD>;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nt, smem) != cudaSuccess)
+        blocks = 1;
+    return std::max(blocks, 1);
+}
+
+// run (occ == nullptr) or query occupancy of the instantiation for (V, rx mod 4, method)
+template <int V>
+static cudaError_t dispatch_rx(int m, bool sv, dim3 grid, int nt, size_t smem,
+                               const SlideParams& p, cudaStream_t st, int* occ) {
+#define DTB_CASE(M)                                                                          \
+    case M:                                                                                  \
+        if (occ) {                                                                           \
+            *occ = sv ? occupancy<V, M, DTB_METHOD_SAUVOLA>(nt, smem)                         \
+                      : occupancy<V, M, DTB_METHOD_NIBLACK>(nt, smem);                        \
+            return cudaSuccess;                                                              \
+        }                                                                                    \
+        return sv ? run_slide<V, M, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st)                \
+                  : run_slide<V, M, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st);
+    switch (m) {
+        DTB_CASE(0)
+        DTB_CASE(1)
+        DTB_CASE(2)
+        DTB_CASE(3)
+    }
+#undef DTB_CASE
+    return cudaErrorInvalidValue;
+}
+
+static int slide_v() {
+    static int v = 0;
+    if (v == 0) {
+        const char* env = getenv("DTB_SLIDE_V");
+        v = (env && atoi(env) == 16) ? 16 : 32;
+    }
+    return v;
+}
+
+cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
+    slide_constants(p);
+    const int V = slide_v();
+    const int rows_out = p.out_end - p.out_begin;
+    const int alpha = (16 - (p.rx & 15)) & 15;
+    // strip plan: w warps -> NC = 32 V w columns; pick the w (1..8) with the least total column
+    // work (strips x NC) for this image width, balancing the strips' output widths.
+    int best_w = 0, best_strips = 0, best_tw = 0;
+    long best_work = 0;
+    for (int w = 1; w <= 8; ++w) {
+        const int nc = 32 * V * w;
+        const int twmax = 32 * ((nc - 2 * p.rx - alpha) / 32);
+        if (twmax < 32) continue;
+        const int ns = (p.cols + twmax - 1) / twmax;
+        const int tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
+        const long work = (long)ns * nc;
+        if (best_w == 0 || work < best_work) {
+            best_w = w; best_strips = ns; best_tw = tw; best_work = work;
+        }
+    }
+    if (best_w == 0) return cudaErrorInvalidValue;  // window too wide for 8 warps (caller checks)
+    const int nt = 32 * best_w;
+    p.NC = V * nt;
+    p.TW = best_tw;
+    const int nstrips = best_strips;
+    const size_t smem = slide_smem_bytes(p.NC);
+    const int m = p.rx & 3;
+    const bool sv = p.method == DTB_METHOD_SAUVOLA;
+    int occ = 1;
+    if (V == 16) dispatch_rx<16>(m, sv, dim3(), nt, smem, p, st, &occ);
+    else dispatch_rx<32>(m, sv, dim3(), nt, smem, p, st, &occ);
+    // bands: one full wave of resident CTAs (bands as tall as possible: the warm-up of each
+    // band costs 2r+1 rows of vertical work)
+    const int slots = num_sms * occ;
+    int nbands = std::max(1, slots / std::max(1, nstrips * n_images));
+    nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
+    p.TH = (rows_out + nbands - 1) / nbands;
+    dim3 grid(nstrips, (rows_out + p.TH - 1) / p.TH, n_images);
+    return V == 16 ? dispatch_rx<16>(m, sv, grid, nt, smem, p, st, nullptr)
+                   : dispatch_rx<32>(m, sv, grid, nt, smem, p, st, nullptr);
+}
+
+}  // namespace dtb

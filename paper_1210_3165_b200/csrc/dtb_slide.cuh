@@ -1,0 +1,48 @@
+// dtb_slide.cuh -- parameters and launcher of the fast sliding-sum binarization kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dtb {
+
+struct SlideParams {
+    const uint8_t* in;
+    int64_t pitch;
+    int64_t img_stride;
+    int cols, row0, H, out_begin, out_end;
+    int r, rx;
+    int NC;     // columns per strip (= 32 * blockDim.x), set by launch_slide
+    int TW;     // outputs per strip (multiple of 32), set by launch_slide
+    int TH;     // output rows per band, set by launch_slide
+    uint8_t* bin;
+    int64_t bin_pitch;
+    int64_t out_stride;
+    int method;
+    double k, rr;
+    uint32_t N;        // (2r+1)^2: count of an unclipped window
+    float cA, cC, tol; // fp32 fast-path constants (for n = N) and certified tolerance
+    float a, c;        // Sauvola: 1-k, k/R; Niblack: 1, k (border constants are rebuilt per n)
+};
+
+#define SLIDE_STAGES 4
+
+// Words of one padded prefix array (logical 16-byte chunk L stored at chunk L + L/8).
+__host__ __device__ inline int slide_padded_words(int NC) {
+    const int chunks = NC / 4 + 4;
+    return 4 * (chunks + chunks / 8 + 1);
+}
+
+// Dynamic shared memory of the fast kernel: 2 padded prefix arrays, warp totals, 2*NS
+// mbarriers, and NS ring stages of (entering, leaving, centre) row segments of NC bytes.
+__host__ __device__ inline size_t slide_smem_bytes(int NC) {
+    return sizeof(uint32_t) * (2 * (size_t)slide_padded_words(NC) + 16) +
+           2 * SLIDE_STAGES * sizeof(uint64_t) + (size_t)SLIDE_STAGES * 3 * NC;
+}
+
+// Fills N / cA / cC / tol from (r, method, k, rr) -- see the error analysis in dtb_slide.cu.
+void slide_constants(SlideParams& p);
+
+cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st);
+
+
+}  // namespace dtb

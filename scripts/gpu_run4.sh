@@ -1,0 +1,6 @@
+set -x
+timeout 900 python -m pytest tests/test_fast_path_gpu.py tests/test_parity_gpu.py -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench.log 2>&1; echo bench=$?
+timeout 600 python bench.py --config c3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3.log 2>&1; echo bench3=$?
+timeout 600 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:slide_kernel -s 2 -c 1 -o gpurun_out/prof_slide python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/ncu.log 2>&1; echo ncu=$?

@@ -1,0 +1,84 @@
+"""Stress the fast certified-decision kernel (dtb_slide.cu) against the CPU oracle:
+many sizes, windows 3..255, both methods, extreme k / R, near-tie-heavy inputs, unaligned
+pitches, band offsets and batches.  Bit-exact binary output is required everywhere."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1210_3165_b200 import engine, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(img, win, method, k, r=128.0):
+    got, _ = engine.binarize(img, win, method, k, r, want_tmap=False)
+    want, _ = oracle.binarize(img, win, method, k, r, tmap=False, threads=8)
+    got = got.cpu().numpy()
+    if not np.array_equal(got, want):
+        bad = np.argwhere(got != want)
+        raise AssertionError(f"{len(bad)} mismatches, first at {bad[:5].tolist()} "
+                             f"(win={win} {method} k={k} r={r} shape={img.shape})")
+
+
+@pytest.mark.parametrize("win", [3, 5, 9, 15, 31, 63, 127, 255])
+def test_documents_all_windows(win):
+    img = workloads.c1_image()
+    for method, k in (("sauvola", 0.5), ("sauvola", 0.05), ("sauvola", 0.9), ("niblack", -0.2),
+                      ("niblack", 0.0), ("niblack", 0.5)):
+        _check(img, win, method, k)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_shapes(seed):
+    rng = np.random.default_rng(seed)
+    for _ in range(6):
+        h, w = int(rng.integers(1, 700)), int(rng.integers(1, 1500))
+        img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+        win = int(rng.choice([3, 7, 21, 33, 65, 129, 255]))
+        _check(img, win, "sauvola", float(rng.choice([0.34, 0.5, 0.2])),
+               float(rng.choice([128.0, 64.0, 200.0])))
+        _check(img, win, "niblack", float(rng.choice([-0.2, 0.0, 0.3])))
+
+
+def test_near_ties_niblack_k0():
+    # t == mean exactly: integer-mean windows make f == t ties common
+    rng = np.random.default_rng(7)
+    img = rng.integers(100, 104, (600, 900)).astype(np.uint8)
+    for win in (3, 5, 15, 31):
+        _check(img, win, "niblack", 0.0)
+        _check(img, win, "sauvola", 1e-9, 1e9)
+
+
+def test_flat_and_extreme_regions():
+    img = np.full((300, 700), 200, np.uint8)
+    img[100:140, 200:260] = 0
+    img[:, 500:] = 255
+    img[250:, :] = 1
+    for win in (3, 15, 63, 127):
+        _check(img, win, "sauvola", 0.34)
+        _check(img, win, "niblack", -0.2)
+
+
+def test_unaligned_pitch_and_bands():
+    torch = engine.torch_mod()
+    img = workloads.c5_image()[:1000, :1500]
+    wide = torch.zeros((1000, 1523), dtype=torch.uint8, device="cuda")
+    wide[:, 7:1507] = torch.from_numpy(img).cuda()
+    view = wide[:, 7:1507]  # pitch 1523, base offset 7: scalar-load path
+    want, _ = oracle.binarize(img, 63, "sauvola", 0.5, tmap=False)
+    got = engine.binarize_band(view, 0, 1000, 0, 1000, 63, "sauvola", 0.5, 128.0)
+    assert np.array_equal(got.cpu().numpy(), want)
+    for y0, y1 in ((0, 1), (13, 500), (999, 1000), (400, 1000)):
+        a, z = max(y0 - 31, 0), min(y1 + 31, 1000)
+        got = engine.binarize_band(view[a:z], a, 1000, y0, y1, 63, "sauvola", 0.5, 128.0)
+        assert np.array_equal(got.cpu().numpy(), want[y0:y1]), (y0, y1)
+
+
+def test_batch_matches_single():
+    torch = engine.torch_mod()
+    imgs = np.stack([workloads.c3_image(i, size=512) for i in range(5)])
+    out = engine.binarize_batch(torch.from_numpy(imgs).cuda(), 31, "niblack", -0.2, 128.0)
+    for i in range(5):
+        assert np.array_equal(out[i].cpu().numpy(),
+                              oracle.binarize(imgs[i], 31, "niblack", -0.2, tmap=False)[0])
