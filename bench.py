@@ -44,7 +44,7 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["c4", "c3", "c5", "c2", "c1"], default="c4")
@@ -76,7 +76,7 @@ class ClockSampler:
     def __init__(self, uuid: str | None):
         self.lines = []
         cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-               "-lms", "200"]
+               "-lms", "50"]
         if uuid:
             cmd += ["-i", uuid]
         try:
@@ -94,7 +94,7 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.06)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
@@ -252,6 +252,7 @@ def run_ours(a):
         if world > 1:
             dist.barrier(device_ids=[local])
 
+    sampler = ClockSampler(None) if rank == 0 else None
     for i in range(a.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -259,7 +260,8 @@ def run_ours(a):
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(a.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(None) if rank == 0 else None
+    if sampler:
+        sampler.lines.clear()  # keep only samples taken during the timed region
     barrier()
     torch.cuda.synchronize()
     t0.record(stream)

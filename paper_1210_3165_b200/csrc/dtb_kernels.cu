@@ -194,14 +194,43 @@ __global__ void __launch_bounds__(NT) strip_kernel(StripParams p) {
     }
 }
 
+// to_gray (pnm.py:18-38), 16 pixels per thread: 3 x 16-byte loads of interleaved RGB, integer
+// 299r+587g+114b with the fp64 re-evaluation only at exact .5 ties (gray_fast), one 16-byte
+// store.  Rows are processed by a grid-stride loop over (row, 16-pixel chunk); ragged row
+// tails and unaligned rows fall back to per-pixel code.
 __global__ void to_gray_kernel(const uint8_t* rgb, int64_t rgb_pitch, uint8_t* gray,
                                int64_t gray_pitch, int rows, int cols) {
-    const int64_t n = (int64_t)rows * cols;
+    const int chunks = (cols + 15) / 16;
+    const int64_t n = (int64_t)rows * chunks;
+    const bool vec = ((reinterpret_cast<uintptr_t>(rgb) | (uintptr_t)rgb_pitch |
+                       reinterpret_cast<uintptr_t>(gray) | (uintptr_t)gray_pitch) & 15) == 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int y = (int)(i / cols), x = (int)(i % cols);
-        const uint8_t* px = rgb + (int64_t)y * rgb_pitch + 3 * (int64_t)x;
-        gray[(int64_t)y * gray_pitch + x] = (uint8_t)gray_fast(px[0], px[1], px[2]);
+        const int y = (int)(i / chunks), x0 = 16 * (int)(i % chunks);
+        const uint8_t* src = rgb + (int64_t)y * rgb_pitch + 3 * (int64_t)x0;
+        uint8_t* dst = gray + (int64_t)y * gray_pitch + x0;
+        if (vec && x0 + 16 <= cols) {
+            uint32_t w[12];
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const uint4 v = __ldg(s4 + q);
+                w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+            }
+            uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int b = 3 * j;
+                const uint32_t r = (w[b >> 2] >> (8 * (b & 3))) & 0xFF;
+                const uint32_t g = (w[(b + 1) >> 2] >> (8 * ((b + 1) & 3))) & 0xFF;
+                const uint32_t bl = (w[(b + 2) >> 2] >> (8 * ((b + 2) & 3))) & 0xFF;
+                o[j >> 2] |= gray_fast(r, g, bl) << (8 * (j & 3));
+            }
+            *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+        } else {
+            for (int j = 0; j < 16 && x0 + j < cols; ++j)
+                dst[j] = (uint8_t)gray_fast(src[3 * j], src[3 * j + 1], src[3 * j + 2]);
+        }
     }
 }
 
@@ -410,7 +439,7 @@ int dtb_to_gray(const uint8_t* rgb, int64_t rgb_pitch, uint8_t* gray, int64_t gr
     if (rows < 0 || cols < 0) return fail(DTB_E_INVALID, "shape: negative size %dx%d", rows, cols);
     if (!rgb || !gray) return fail(DTB_E_INVALID, "null image pointer");
     if (rows == 0 || cols == 0) return DTB_OK;
-    const int64_t n = (int64_t)rows * cols;
+    const int64_t n = (int64_t)rows * ((cols + 15) / 16);
     const int threads = 256;
     const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, (int64_t)num_sms() * 16);
     to_gray_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(rgb, rgb_pitch, gray,

@@ -539,28 +539,46 @@ void slide_constants(SlideParams& p) {
     p.tol = (float)(2.0 * (e_ref + e_fast) + 1e-6);
 }
 
+// Host-side launch state is cached per instantiation: the dynamic-smem opt-in is raised once to
+// the largest size ever requested, and occupancy answers are memoised per (block, smem) -- the
+// runtime queries cost tens of microseconds, which would dominate small images.
+template <int V, int RXM4, int METHOD>
+static cudaError_t ensure_smem(size_t smem) {
+    static size_t granted = 48 * 1024;
+    if (smem <= granted) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(slide_kernel<V, RXM4, METHOD>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) granted = smem;
+    return e;
+}
+
 template <int V, int RXM4, int METHOD>
 static cudaError_t run_slide(dim3 grid, int nt, size_t smem, const SlideParams& p,
                              cudaStream_t st) {
-    auto kern = slide_kernel<V, RXM4, METHOD>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    kern<<<grid, nt, smem, st>>>(p);
+    cudaError_t e = ensure_smem<V, RXM4, METHOD>(smem);
+    if (e != cudaSuccess) return e;
+    slide_kernel<V, RXM4, METHOD><<<grid, nt, smem, st>>>(p);
     return cudaGetLastError();
 }
 
 template <int V, int RXM4, int METHOD>
 static int occupancy(int nt, size_t smem) {
+    static int cache_nt[16], cache_occ[16];
+    static size_t cache_smem[16];
+    static int n_cached = 0;
+    for (int i = 0; i < n_cached; ++i)
+        if (cache_nt[i] == nt && cache_smem[i] == smem) return cache_occ[i];
     int blocks = 0;
-    auto kern = slide_kernel<V, RXM4, METHOD>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nt, smem) != cudaSuccess)
+    ensure_smem<V, RXM4, METHOD>(smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, slide_kernel<V, RXM4, METHOD>, nt,
+                                                      smem) != cudaSuccess)
         blocks = 1;
-    return std::max(blocks, 1);
+    blocks = std::max(blocks, 1);
+    if (n_cached < 16) {
+        cache_nt[n_cached] = nt; cache_smem[n_cached] = smem; cache_occ[n_cached] = blocks;
+        ++n_cached;
+    }
+    return blocks;
 }
 
 // run (occ == nullptr) or query occupancy of the instantiation for (V, rx mod 4, method)
