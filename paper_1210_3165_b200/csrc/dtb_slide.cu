@@ -32,10 +32,19 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "docthresh_b200.h"
 #include "dtb_common.cuh"
 #include "dtb_slide.cuh"
+
+// Tuning switches (measured on B200, C4: quarters 0.662 vs 0.684 ms; a 3-lane producer 0.73 ms)
+#ifndef DTB_PREFIX_QUARTERS
+#define DTB_PREFIX_QUARTERS 1
+#endif
+#ifndef DTB_PAR_PRODUCER
+#define DTB_PAR_PRODUCER 0
+#endif
 
 namespace dtb {
 
@@ -256,10 +265,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+// L2 eviction priorities: a row is read three times (entering, centre r steps later, leaving
+// 2r+1 steps later); keep it resident on the first two reads, let it go on the last.
+__device__ __forceinline__ uint64_t make_policy(int kind) {
+    uint64_t p;
+    if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 
 // Sequence of pipeline items for one CTA: warm-up rows g0..g1 (entering row only), then
@@ -329,7 +349,10 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     // producer (thread 0): stage item k.  Rows outside the image are not copied; consumers
     // treat them as zero.  The byte tail beyond the last 16-byte chunk is written by thread 0
     // with generic stores (visible to consumers after the barriers in between).
-    auto issue = [&](int k) {
+    const uint64_t pol_keep = make_policy(p.l2hint ? 2 : 0), pol_drop = make_policy(p.l2hint ? 1 : 0);
+    // Lanes 0..2 of warp 0 issue the entering / leaving / centre copies in parallel; lane 0 also
+    // arms the full barrier with the byte count (tx-count may transiently go negative).
+    auto issue = [&](int k, int which) {
         const int s = k % NS;
         if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
         uint8_t* E = ring + (size_t)s * 3 * p.NC;
@@ -345,32 +368,55 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             go = (k == it.nwarm) ? -1 : y - p.r - 1;
             if (ge >= p.H) ge = -1;
         }
-        uint32_t bytes = 0;
         const uint32_t rowb = (uint32_t)(c_hi16 - c_lo), fb = (uint32_t)(f_hi16 - X0);
-        if (ge >= 0) bytes += rowb;
-        if (go >= 0) bytes += rowb;
-        if (gf >= 0) bytes += fb;
-        mbar_expect_tx(&full[s], bytes);
-        if (ge >= 0 && rowb) bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s]);
-        if (go >= 0 && rowb) bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s]);
-        if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s]);
-        for (int c = c_hi16; c < c_hi; ++c) {
-            if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
-            if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+        if (!DTB_PAR_PRODUCER) {
+            uint32_t bytes = 0;
+            if (ge >= 0) bytes += rowb;
+            if (go >= 0) bytes += rowb;
+            if (gf >= 0) bytes += fb;
+            mbar_expect_tx(&full[s], bytes);
+            if (ge >= 0 && rowb)
+                bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s], pol_keep);
+            if (go >= 0 && rowb)
+                bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s], pol_drop);
+            if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s], pol_keep);
+            for (int c = c_hi16; c < c_hi; ++c) {
+                if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
+                if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+            }
+            for (int c = f_hi16; c < f_hi; ++c)
+                if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+        } else if (which == 0) {
+            uint32_t bytes = 0;
+            if (ge >= 0) bytes += rowb;
+            if (go >= 0) bytes += rowb;
+            if (gf >= 0) bytes += fb;
+            mbar_expect_tx(&full[s], bytes);
+            if (ge >= 0 && rowb)
+                bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s], pol_keep);
+            for (int c = c_hi16; c < c_hi; ++c) {
+                if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
+                if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+            }
+            for (int c = f_hi16; c < f_hi; ++c)
+                if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+        } else if (which == 1) {
+            if (go >= 0 && rowb)
+                bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s], pol_drop);
+        } else {
+            if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s], pol_keep);
         }
-        for (int c = f_hi16; c < f_hi; ++c)
-            if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
     };
-    // lookahead of NS-1 items: item k+NS-1 reuses the stage of item k-1, which every warp has
-    // released by the time thread 0 passes the first barrier of step k (main steps) -- so the
-    // producer never waits on the slowest warp while holding the barrier up.
-    if (t == 0)
-        for (int k = 0; k < min(NS - 1, it.n); ++k) issue(k);
+    const bool producer = DTB_PAR_PRODUCER ? (warp == 0 && lane < 3) : (t == 0);
+    if (producer)
+        for (int k = 0; k < min(NS - 1, it.n); ++k) issue(k, lane);
 
     uint32_t cS[V], cQ[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) { cS[j] = 0; cQ[j] = 0; }
-    uint32_t TS = 0, TQ = 0;  // thread totals sum_j cS[j], sum_j cQ[j], kept incrementally
+    // per-quarter totals of cS / cQ (V/4 columns each), kept incrementally: the thread total
+    // feeds the scan, and the quarter totals let the prefix run as 4 independent chains
+    uint32_t qS[4] = {0, 0, 0, 0}, qQ[4] = {0, 0, 0, 0};
 
     const int xo = X0 + V * t;  // this thread's V output columns
     const bool has_out = (V * t + V + 2 * p.rx + alpha <= p.NC) && (V * t < p.TW) &&
@@ -411,10 +457,10 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             cQ[j] += v * v;
         }
         release(k);
-        if (t == 0 && k + NS - 1 < it.n) issue(k + NS - 1);
+        if (producer && k + NS - 1 < it.n) issue(k + NS - 1, lane);
     }
 #pragma unroll
-    for (int j = 0; j < V; ++j) { TS += cS[j]; TQ += cQ[j]; }
+    for (int j = 0; j < V; ++j) { qS[j / (V / 4)] += cS[j]; qQ[j / (V / 4)] += cQ[j]; }
 
     for (int k = it.nwarm; k < it.n; ++k) {
         const int y = it.ya + (k - it.nwarm);
@@ -444,13 +490,16 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             }
 #pragma unroll
             for (int q = 0; q < V / 4; ++q) {  // 4 columns per dp4a: sum of bytes / of squares
-                TS += (uint32_t)__dp4a(e[q], 0x01010101u, 0u) - (uint32_t)__dp4a(o[q], 0x01010101u, 0u);
-                TQ += (uint32_t)__dp4a(e[q], e[q], 0u) - (uint32_t)__dp4a(o[q], o[q], 0u);
+                qS[q / (V / 16)] += (uint32_t)__dp4a(e[q], 0x01010101u, 0u) -
+                                    (uint32_t)__dp4a(o[q], 0x01010101u, 0u);
+                qQ[q / (V / 16)] += (uint32_t)__dp4a(e[q], e[q], 0u) - (uint32_t)__dp4a(o[q], o[q], 0u);
             }
         }
 
         // ---- horizontal inclusive prefix, exact mod 2^32 (lanes >= the warp's live count
         // never exist: blockDim is a multiple of 32)
+        const uint32_t TS = (qS[0] + qS[1]) + (qS[2] + qS[3]);
+        const uint32_t TQ = (qQ[0] + qQ[1]) + (qQ[2] + qQ[3]);
         uint32_t iS = TS, iQ = TQ;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -460,9 +509,38 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
         }
         if (lane == 31) { sWS[warp] = iS; sWQ[warp] = iQ; }
         __syncthreads();
-        if (t == 0 && k + NS - 1 < it.n) issue(k + NS - 1);
+        if (producer && k + NS - 1 < it.n) issue(k + NS - 1, lane);
         uint32_t bS = iS - TS, bQ = iQ - TQ;
         for (int w = 0; w < warp; ++w) { bS += sWS[w]; bQ += sWQ[w]; }
+#if DTB_PREFIX_QUARTERS
+        // logical word Vt + m holds P[Vt + m - 1]: the first slot is this thread's base.
+        // Four independent running chains, one per quarter of the thread's columns.
+        uint32_t cbS[4], cbQ[4];
+        cbS[0] = bS; cbQ[0] = bQ;
+#pragma unroll
+        for (int h = 1; h < 4; ++h) { cbS[h] = cbS[h - 1] + qS[h - 1]; cbQ[h] = cbQ[h - 1] + qQ[h - 1]; }
+        bS = cbS[3] + qS[3];
+        bQ = cbQ[3] + qQ[3];
+#pragma unroll
+        for (int j = 0; j < V / 4; j += 4) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int c0 = h * (V / 4) + j;
+                uint4 vs, vq;
+                vs.x = cbS[h]; vq.x = cbQ[h];
+                cbS[h] += cS[c0]; cbQ[h] += cQ[c0];
+                vs.y = cbS[h]; vq.y = cbQ[h];
+                cbS[h] += cS[c0 + 1]; cbQ[h] += cQ[c0 + 1];
+                vs.z = cbS[h]; vq.z = cbQ[h];
+                cbS[h] += cS[c0 + 2]; cbQ[h] += cQ[c0 + 2];
+                vs.w = cbS[h]; vq.w = cbQ[h];
+                cbS[h] += cS[c0 + 3]; cbQ[h] += cQ[c0 + 3];
+                const int pw = pchunk_word((V / 4) * t + c0 / 4);
+                *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
+                *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
+            }
+        }
+#else
         // logical word Vt + m holds P[Vt + m - 1]: the first slot is this thread's base
 #pragma unroll
         for (int j = 0; j < V; j += 4) {
@@ -479,6 +557,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
             *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
         }
+#endif
         if (t == blockDim.x - 1) {  // logical word NC = P[NC - 1]
             const int pw = pchunk_word(p.NC / 4);
             sPS[pw] = bS;
@@ -516,6 +595,8 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
 // rounding of D, sqrt.approx / rcp.approx (<= 2^-21 assumed each), the rounded constants and
 // the fmas give a relative error <= 1.1e-6 on the threshold; we use 1.5e-6 times a bound on |t|.
 void slide_constants(SlideParams& p) {
+    const char* env = getenv("DTB_L2HINT");
+    p.l2hint = env ? atoi(env) : 1;
     const double W = 2.0 * p.r + 1.0, N = W * W;
     p.N = (uint32_t)N;
     const double sd_err = 6.6e-6, rel = 1.5e-6;

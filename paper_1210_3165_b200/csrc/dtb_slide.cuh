@@ -22,6 +22,7 @@ struct SlideParams {
     uint32_t N;        // (2r+1)^2: count of an unclipped window
     float cA, cC, tol; // fp32 fast-path constants (for n = N) and certified tolerance
     float a, c;        // Sauvola: 1-k, k/R; Niblack: 1, k (border constants are rebuilt per n)
+    int l2hint;        // 1: evict_last / evict_first L2 policies on the staged row copies
 };
 
 #define SLIDE_STAGES 4
