@@ -42,6 +42,19 @@
 #ifndef DTB_PREFIX_QUARTERS
 #define DTB_PREFIX_QUARTERS 1
 #endif
+#ifndef DTB_WS_DEFAULT
+#define DTB_WS_DEFAULT 2  // 0 classic, 1 always warp-specialized, 2 auto
+#endif
+#ifndef DTB_ALU_BALANCE
+#define DTB_ALU_BALANCE 0
+#endif
+// diagnostics only (wrong results): 1 = skip the output phase, 2 = skip prefix stores
+#ifndef DTB_DIAG_SKIP
+#define DTB_DIAG_SKIP 0
+#endif
+#ifndef DTB_D_SPLIT
+#define DTB_D_SPLIT 0
+#endif
 #ifndef DTB_PAR_PRODUCER
 #define DTB_PAR_PRODUCER 0
 #endif
@@ -114,7 +127,13 @@ template <int METHOD, bool BORDER>
 __device__ __forceinline__ float fast_diff(uint32_t S, uint32_t Q, uint32_t f, uint32_t n,
                                            float cA, float cC, float a, float c) {
     const uint64_t D = (uint64_t)n * Q - (uint64_t)S * S;  // exact, >= 0
-    const float sD = sqrt_ftz((float)D);
+#if DTB_D_SPLIT
+    // D < 2^49: hi*2^32 + lo with two full-rate I2FP conversions and one FFMA (rel. err 2^-23)
+    const float Df = __fmaf_rn((float)(uint32_t)(D >> 32), 4294967296.0f, (float)(uint32_t)D);
+#else
+    const float Df = (float)D;  // I2F.U64 (XU pipe)
+#endif
+    const float sD = sqrt_ftz(Df);
     const float Sf = (float)S;
     if (BORDER) {
         const float rn = rcp_ftz((float)n);
@@ -173,9 +192,8 @@ __device__ __noinline__ void fix_uncertain(const uint32_t* sPS, const uint32_t* 
 template <int V, int RXM4, int METHOD, bool BORDER>
 __device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t* sPQ,
                                             const int (&aw)[V / 4 + 1], const int (&bw)[V / 4 + 1],
-                                            const uint8_t* fsm, uint8_t* orow, int xo,
-                                            int cols, bool full, int ny, int r,
-                                            const SlideParams& p) {
+                                            const uint8_t* fsm, uint32_t (&ow)[V / 4], int xo,
+                                            int cols, int ny, int r, const SlideParams& p) {
     constexpr int MA = (4 - RXM4) & 3;  // misalignment (words) of the A run
     constexpr int MB = (RXM4 + 1) & 3;  // misalignment (words) of the B run
     uint32_t fw[V / 4];  // row y pixel values of this thread's V outputs, from the shared stage
@@ -185,7 +203,6 @@ __device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t*
         fw[4 * q] = v.x; fw[4 * q + 1] = v.y; fw[4 * q + 2] = v.z; fw[4 * q + 3] = v.w;
     }
     float mind = 3.0e38f;
-    uint32_t ow[V / 4];
 #pragma unroll
     for (int g = 0; g < V / 8; ++g) {  // groups of 8 outputs
         uint32_t S8[8], Q8[8];
@@ -228,18 +245,6 @@ __device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t*
                           prmt(__float_as_uint(d[2]), __float_as_uint(d[3]), 0xFBFB), 0x5410);
         ow[2 * g + 1] = ~prmt(prmt(__float_as_uint(d[4]), __float_as_uint(d[5]), 0xFBFB),
                               prmt(__float_as_uint(d[6]), __float_as_uint(d[7]), 0xFBFB), 0x5410);
-    }
-    if (full) {
-#pragma unroll
-        for (int q = 0; q < V / 16; ++q)
-            *reinterpret_cast<uint4*>(orow + xo + 16 * q) =
-                make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int x = xo + j;
-            if (x >= 0 && x < cols) orow[x] = (uint8_t)(ow[j >> 2] >> (8 * (j & 3)));
-        }
     }
     return mind < p.tol;
 }
@@ -467,37 +472,30 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
         const int s = k % NS;
         mbar_wait(&full[s], (k / NS) & 1);
         const uint8_t* stage = ring + (size_t)s * 3 * p.NC;
-        if (k > it.nwarm) {
-            const bool ein = y + p.r < p.H, oin = y - p.r - 1 >= 0;
-            uint32_t e[V / 4], o[V / 4];
-            {
-                const uint4* E = reinterpret_cast<const uint4*>(stage + V * t);
-                const uint4* O = reinterpret_cast<const uint4*>(stage + p.NC + V * t);
+        // Entering / leaving rows (all-zero on the band's first step and past the image), the
+        // dp4a totals, the warp scan and the per-column vertical update form ONE basic block:
+        // the scan's shuffle latency is hidden behind the independent column updates.
+        const bool first = (k == it.nwarm);
+        const bool ein = !first && y + p.r < p.H, oin = !first && y - p.r - 1 >= 0;
+        uint32_t e[V / 4], o[V / 4];
+        {
+            const uint4* E = reinterpret_cast<const uint4*>(stage + V * t);
+            const uint4* O = reinterpret_cast<const uint4*>(stage + p.NC + V * t);
 #pragma unroll
-                for (int q = 0; q < V / 16; ++q) {
-                    const uint4 a = ein ? E[q] : make_uint4(0, 0, 0, 0);
-                    const uint4 b = oin ? O[q] : make_uint4(0, 0, 0, 0);
-                    e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
-                    o[4 * q] = b.x; o[4 * q + 1] = b.y; o[4 * q + 2] = b.z; o[4 * q + 3] = b.w;
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < V; ++j) {
-                const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
-                const uint32_t dv = ev - ov;
-                cS[j] += dv;
-                cQ[j] += dv * (ev + ov);
-            }
-#pragma unroll
-            for (int q = 0; q < V / 4; ++q) {  // 4 columns per dp4a: sum of bytes / of squares
-                qS[q / (V / 16)] += (uint32_t)__dp4a(e[q], 0x01010101u, 0u) -
-                                    (uint32_t)__dp4a(o[q], 0x01010101u, 0u);
-                qQ[q / (V / 16)] += (uint32_t)__dp4a(e[q], e[q], 0u) - (uint32_t)__dp4a(o[q], o[q], 0u);
+            for (int q = 0; q < V / 16; ++q) {
+                const uint4 a = ein ? E[q] : make_uint4(0, 0, 0, 0);
+                const uint4 b = oin ? O[q] : make_uint4(0, 0, 0, 0);
+                e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
+                o[4 * q] = b.x; o[4 * q + 1] = b.y; o[4 * q + 2] = b.z; o[4 * q + 3] = b.w;
             }
         }
-
-        // ---- horizontal inclusive prefix, exact mod 2^32 (lanes >= the warp's live count
-        // never exist: blockDim is a multiple of 32)
+#pragma unroll
+        for (int q = 0; q < V / 4; ++q) {  // 4 columns per dp4a: sum of bytes / of squares
+            qS[q / (V / 16)] += (uint32_t)__dp4a(e[q], 0x01010101u, 0u) -
+                                (uint32_t)__dp4a(o[q], 0x01010101u, 0u);
+            qQ[q / (V / 16)] += (uint32_t)__dp4a(e[q], e[q], 0u) - (uint32_t)__dp4a(o[q], o[q], 0u);
+        }
+        // ---- horizontal inclusive prefix, exact mod 2^32 (blockDim is a multiple of 32)
         const uint32_t TS = (qS[0] + qS[1]) + (qS[2] + qS[3]);
         const uint32_t TQ = (qQ[0] + qQ[1]) + (qQ[2] + qQ[3]);
         uint32_t iS = TS, iQ = TQ;
@@ -506,6 +504,20 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
             const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
             if (lane >= off) { iS += vs; iQ += vq; }
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
+#if DTB_ALU_BALANCE
+            cS[j] = cS[j] + ev - ov;                 // IADD3 (ALU pipe)
+            const uint32_t nov = 0u - ov;            // IADD3
+            cQ[j] = ev * ev + cQ[j];                 // IMAD
+            cQ[j] = nov * ov + cQ[j];                // IMAD
+#else
+            const uint32_t dv = ev - ov;
+            cS[j] += dv;
+            cQ[j] += dv * (ev + ov);
+#endif
         }
         if (lane == 31) { sWS[warp] = iS; sWQ[warp] = iQ; }
         __syncthreads();
@@ -527,6 +539,14 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             for (int h = 0; h < 4; ++h) {
                 const int c0 = h * (V / 4) + j;
                 uint4 vs, vq;
+#if DTB_ALU_BALANCE
+                // P[j+1] = P[j-1] + c[j] + c[j+1]: 3-input adds (IADD3) halve the chain depth
+                vs.x = cbS[h]; vq.x = cbQ[h];
+                vs.y = cbS[h] + cS[c0]; vq.y = cbQ[h] + cQ[c0];
+                vs.z = cbS[h] + cS[c0] + cS[c0 + 1]; vq.z = cbQ[h] + cQ[c0] + cQ[c0 + 1];
+                vs.w = vs.y + cS[c0 + 1] + cS[c0 + 2]; vq.w = vq.y + cQ[c0 + 1] + cQ[c0 + 2];
+                cbS[h] = vs.z + cS[c0 + 2] + cS[c0 + 3]; cbQ[h] = vq.z + cQ[c0 + 2] + cQ[c0 + 3];
+#else
                 vs.x = cbS[h]; vq.x = cbQ[h];
                 cbS[h] += cS[c0]; cbQ[h] += cQ[c0];
                 vs.y = cbS[h]; vq.y = cbQ[h];
@@ -535,9 +555,12 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
                 cbS[h] += cS[c0 + 2]; cbQ[h] += cQ[c0 + 2];
                 vs.w = cbS[h]; vq.w = cbQ[h];
                 cbS[h] += cS[c0 + 3]; cbQ[h] += cQ[c0 + 3];
+#endif
                 const int pw = pchunk_word((V / 4) * t + c0 / 4);
-                *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
-                *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
+                if (!(DTB_DIAG_SKIP & 2)) {
+                    *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
+                    *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
+                }
             }
         }
 #else
@@ -566,24 +589,356 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
         __syncthreads();
 
         // ---- outputs
-        if (has_out) {
+        if (has_out && !(DTB_DIAG_SKIP & 1)) {
             const bool y_interior = (y - p.r >= 0) && (y + p.r <= p.H - 1);
             uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
             const int ny = min(y + p.r, p.H - 1) - max(y - p.r, 0) + 1;
             const uint8_t* fsm = stage + 2 * p.NC + V * t;
             bool unc;
+            uint32_t ow[V / 4];
             if (y_interior && !x_border_warp)
-                unc = row_outputs<V, RXM4, METHOD, false>(sPS, sPQ, aw, bw, fsm, orow, xo, p.cols,
-                                                       out_full, ny, p.r, p);
+                unc = row_outputs<V, RXM4, METHOD, false>(sPS, sPQ, aw, bw, fsm, ow, xo, p.cols, ny,
+                                                          p.r, p);
             else
-                unc = row_outputs<V, RXM4, METHOD, true>(sPS, sPQ, aw, bw, fsm, orow, xo, p.cols,
-                                                      out_full, ny, p.r, p);
+                unc = row_outputs<V, RXM4, METHOD, true>(sPS, sPQ, aw, bw, fsm, ow, xo, p.cols, ny,
+                                                         p.r, p);
+            if (out_full) {
+#pragma unroll
+                for (int q = 0; q < V / 16; ++q)  // streaming store: the output is not re-read
+                    __stcs(reinterpret_cast<uint4*>(orow + xo + 16 * q),
+                           make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    const int x = xo + j;
+                    if (x >= 0 && x < p.cols) orow[x] = (uint8_t)(ow[j >> 2] >> (8 * (j & 3)));
+                }
+            }
             if (__builtin_expect(unc, 0))
                 fix_uncertain<METHOD>(sPS, sPQ, alpha + V * t, alpha + 2 * p.rx + 1 + V * t,
                                       in0 + (int64_t)y * p.pitch, orow, xo, V, p.cols, ny, p.r, p.N,
                                       p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
         }
         release(k);
+    }
+}
+
+
+// =====================================================================================
+// Warp-specialized variant (ws_kernel): column warps (vertical sums + horizontal prefix)
+// and output warps (window sums -> certified decision -> bytes) run CONCURRENTLY on a
+// double-buffered prefix.  Hand-off with named barriers: READY[b] (column -> output: P_k in
+// buffer b = k&1 is complete) and FREE[b] (output -> column: row k-2 consumed, buffer b may
+// be overwritten).  Column warps never wait for the latency-bound output phase of the same
+// row, and output warps never sit behind the column warps' scan / barriers.
+// =====================================================================================
+// Barrier ids are immediates (a register id makes ptxas reserve all 16 barriers, which caps
+// resident CTAs per SM); callers pass (base, buffer) and we branch to constant ids.
+template <int ID>
+__device__ __forceinline__ void nbar_sync_c(int count) {
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(count) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void nbar_arrive_c(int count) {
+    asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+    switch (id) {
+        case 1: nbar_sync_c<1>(count); break;
+        case 2: nbar_sync_c<2>(count); break;
+        case 3: nbar_sync_c<3>(count); break;
+        case 4: nbar_sync_c<4>(count); break;
+        default: nbar_sync_c<5>(count); break;
+    }
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+    switch (id) {
+        case 2: nbar_arrive_c<2>(count); break;
+        case 3: nbar_arrive_c<3>(count); break;
+        case 4: nbar_arrive_c<4>(count); break;
+        default: nbar_arrive_c<5>(count); break;
+    }
+}
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
+}
+
+enum { BAR_COLS = 1, BAR_READY0 = 2, BAR_FREE0 = 4 };
+
+#ifndef DTB_WS_MAXREG
+#define DTB_WS_MAXREG 168
+#endif
+
+template <int VO, int RXM4, int METHOD>
+__global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
+    constexpr int V = 32;  // columns per column thread (VO: outputs per output thread)
+    constexpr int MA = (4 - RXM4) & 3;
+    constexpr int MB = (RXM4 + 1) & 3;
+    constexpr int NS = SLIDE_STAGES;
+    extern __shared__ __align__(128) uint32_t sm[];
+    const int NCp = slide_padded_words(p.NC);
+    uint32_t* sWS = sm + 4 * NCp;   // [2][8] per-column-warp totals, double buffered
+    uint32_t* sWQ = sWS + 16;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sWS + 32);
+    uint64_t* empty = full + NS;
+    uint8_t* ring = reinterpret_cast<uint8_t*>(empty + NS);
+    const int ncw = p.ncw, now = p.now, nthr = 32 * (ncw + now);
+
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const bool is_col = warp < ncw;
+    const uint8_t* in = p.in + (int64_t)blockIdx.z * p.img_stride;
+    const int X0 = (int)blockIdx.x * p.TW;
+    const int alpha = (16 - (p.rx & 15)) & 15;
+    const int xc0 = X0 - p.rx - alpha;
+    const int ya = p.out_begin + (int)blockIdx.y * p.TH;
+    const int yb = min(ya + p.TH, p.out_end);
+    if (ya >= yb) return;
+    const uint8_t* in0 = in - (int64_t)p.row0 * p.pitch;
+    const int c_lo = max(xc0, 0);
+    const int c_hi = min(xc0 + p.NC, p.cols);
+    const int c_hi16 = c_lo + ((max(c_hi - c_lo, 0)) & ~15);
+    const int f_hi = min(X0 + p.TW, p.cols);
+    const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
+    Items it;
+    it.g0 = max(ya - p.r, 0);
+    it.nwarm = min(ya + p.r, p.H - 1) - it.g0 + 1;
+    it.ya = ya;
+    it.n = it.nwarm + (yb - ya);
+
+    {
+        uint4* r4 = reinterpret_cast<uint4*>(ring);
+        const int n16 = NS * 3 * p.NC / 16;
+        for (int i = t; i < n16; i += blockDim.x) r4[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], ncw + now);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint64_t pol_keep = make_policy(p.l2hint ? 2 : 0), pol_drop = make_policy(p.l2hint ? 1 : 0);
+    auto issue = [&](int k) {
+        const int s = k % NS;
+        if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
+        uint8_t* E = ring + (size_t)s * 3 * p.NC;
+        uint8_t* O = E + p.NC;
+        uint8_t* F = O + p.NC;
+        int ge, go = -1, gf = -1;
+        if (k < it.nwarm) {
+            ge = it.g0 + k;
+        } else {
+            const int y = it.ya + (k - it.nwarm);
+            gf = y;
+            ge = (k == it.nwarm) ? -1 : y + p.r;
+            go = (k == it.nwarm) ? -1 : y - p.r - 1;
+            if (ge >= p.H) ge = -1;
+        }
+        const uint32_t rowb = (uint32_t)(c_hi16 - c_lo), fb = (uint32_t)(f_hi16 - X0);
+        uint32_t bytes = 0;
+        if (ge >= 0) bytes += rowb;
+        if (go >= 0) bytes += rowb;
+        if (gf >= 0) bytes += fb;
+        mbar_expect_tx(&full[s], bytes);
+        if (ge >= 0 && rowb)
+            bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s], pol_keep);
+        if (go >= 0 && rowb)
+            bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s], pol_drop);
+        if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s], pol_keep);
+        for (int c = c_hi16; c < c_hi; ++c) {
+            if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
+            if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+        }
+        for (int c = f_hi16; c < f_hi; ++c)
+            if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+    };
+
+    if (is_col) {
+        // ===================== column warps =====================
+        int issued = 0;
+        if (t == 0)
+            while (issued < min(NS - 1, it.n)) issue(issued++);
+        uint32_t cS[V], cQ[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) { cS[j] = 0; cQ[j] = 0; }
+        uint32_t qS[4] = {0, 0, 0, 0}, qQ[4] = {0, 0, 0, 0};
+        for (int k = 0; k < it.nwarm; ++k) {
+            const int s = k % NS;
+            mbar_wait(&full[s], (k / NS) & 1);
+            const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + V * t);
+            uint32_t w[V / 4];
+#pragma unroll
+            for (int q = 0; q < V / 16; ++q) {
+                const uint4 a = E[q];
+                w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+            }
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const uint32_t v = byte_at(w, j);
+                cS[j] += v;
+                cQ[j] += v * v;
+            }
+            __syncwarp();
+            // warm-up items are not read by output warps: warp 0 arrives for them as well
+            if (lane == 0) mbar_arrive_cnt(&empty[s], warp == 0 ? 1 + now : 1);
+            if (t == 0)
+                while (issued < min(k + NS, it.n)) issue(issued++);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) { qS[j / (V / 4)] += cS[j]; qQ[j / (V / 4)] += cQ[j]; }
+
+        for (int k = it.nwarm; k < it.n; ++k) {
+            const int y = it.ya + (k - it.nwarm);
+            const int s = k % NS;
+            const int b = (k - it.nwarm) & 1;
+            mbar_wait(&full[s], (k / NS) & 1);
+            const uint8_t* stage = ring + (size_t)s * 3 * p.NC;
+            const bool first = (k == it.nwarm);
+            const bool ein = !first && y + p.r < p.H, oin = !first && y - p.r - 1 >= 0;
+            uint32_t e[V / 4], o[V / 4];
+            {
+                const uint4* E = reinterpret_cast<const uint4*>(stage + V * t);
+                const uint4* O = reinterpret_cast<const uint4*>(stage + p.NC + V * t);
+#pragma unroll
+                for (int q = 0; q < V / 16; ++q) {
+                    const uint4 a = ein ? E[q] : make_uint4(0, 0, 0, 0);
+                    const uint4 bb = oin ? O[q] : make_uint4(0, 0, 0, 0);
+                    e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
+                    o[4 * q] = bb.x; o[4 * q + 1] = bb.y; o[4 * q + 2] = bb.z; o[4 * q + 3] = bb.w;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < V / 4; ++q) {
+                qS[q / (V / 16)] += (uint32_t)__dp4a(e[q], 0x01010101u, 0u) -
+                                    (uint32_t)__dp4a(o[q], 0x01010101u, 0u);
+                qQ[q / (V / 16)] += (uint32_t)__dp4a(e[q], e[q], 0u) - (uint32_t)__dp4a(o[q], o[q], 0u);
+            }
+            const uint32_t TS = (qS[0] + qS[1]) + (qS[2] + qS[3]);
+            const uint32_t TQ = (qQ[0] + qQ[1]) + (qQ[2] + qQ[3]);
+            uint32_t iS = TS, iQ = TQ;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
+                const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
+                if (lane >= off) { iS += vs; iQ += vq; }
+            }
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
+                const uint32_t dv = ev - ov;
+                cS[j] += dv;
+                cQ[j] += dv * (ev + ov);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with item k's rows
+            if (lane == 31) { sWS[8 * b + warp] = iS; sWQ[8 * b + warp] = iQ; }
+            nbar_sync(BAR_COLS, 32 * ncw);
+            uint32_t bS = iS - TS, bQ = iQ - TQ;
+            for (int w = 0; w < warp; ++w) { bS += sWS[8 * b + w]; bQ += sWQ[8 * b + w]; }
+            // wait until the output warps have consumed row k-2 from this prefix buffer
+            nbar_sync(BAR_FREE0 + b, nthr);
+            if (t == 0)
+                while (issued < min(k + NS - 1, it.n)) issue(issued++);
+            uint32_t* sPS = sm + (2 * b) * NCp;
+            uint32_t* sPQ = sm + (2 * b + 1) * NCp;
+            uint32_t cbS[4], cbQ[4];
+            cbS[0] = bS; cbQ[0] = bQ;
+#pragma unroll
+            for (int h = 1; h < 4; ++h) { cbS[h] = cbS[h - 1] + qS[h - 1]; cbQ[h] = cbQ[h - 1] + qQ[h - 1]; }
+#pragma unroll
+            for (int j = 0; j < V / 4; j += 4) {
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int c0 = h * (V / 4) + j;
+                    uint4 vs, vq;
+                    vs.x = cbS[h]; vq.x = cbQ[h];
+                    cbS[h] += cS[c0]; cbQ[h] += cQ[c0];
+                    vs.y = cbS[h]; vq.y = cbQ[h];
+                    cbS[h] += cS[c0 + 1]; cbQ[h] += cQ[c0 + 1];
+                    vs.z = cbS[h]; vq.z = cbQ[h];
+                    cbS[h] += cS[c0 + 2]; cbQ[h] += cQ[c0 + 2];
+                    vs.w = cbS[h]; vq.w = cbQ[h];
+                    cbS[h] += cS[c0 + 3]; cbQ[h] += cQ[c0 + 3];
+                    const int pw = pchunk_word((V / 4) * t + c0 / 4);
+                    *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
+                    *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
+                }
+            }
+            if (t == 32 * ncw - 1) {  // logical word NC = P[NC - 1]
+                const int pw = pchunk_word(p.NC / 4);
+                sPS[pw] = cbS[3];
+                sPQ[pw] = cbQ[3];
+            }
+            nbar_arrive(BAR_READY0 + b, nthr);
+        }
+        // consume the output warps' last FREE arrivals so no named barrier is left pending
+        const int rows = it.n - it.nwarm;
+        if (rows >= 1) nbar_sync(BAR_FREE0 + (rows & 1), nthr);
+        if (rows >= 2) nbar_sync(BAR_FREE0 + ((rows + 1) & 1), nthr);
+    } else {
+        // ===================== output warps =====================
+        const int to = t - 32 * ncw;  // output thread index
+        const int xo = X0 + VO * to;
+        const bool has_out = (VO * to + VO + 2 * p.rx + alpha <= p.NC) && (VO * to < p.TW) &&
+                             (xo < p.cols);
+        const bool out_full = has_out && (xo + VO <= p.cols) &&
+                              ((reinterpret_cast<uintptr_t>(p.bin) | (uintptr_t)p.bin_pitch |
+                                (uintptr_t)p.out_stride) & 15) == 0;
+        const bool x_interior = (p.rx == p.r) && (xo - p.r >= 0) && (xo + VO - 1 + p.r <= p.cols - 1);
+        const int la0 = (alpha + VO * to - MA) >> 2;
+        const int lb0 = (alpha + 2 * p.rx + 1 + VO * to - MB) >> 2;
+        int aw[VO / 4 + 1], bw[VO / 4 + 1];
+#pragma unroll
+        for (int i = 0; i < VO / 4 + 1; ++i) { aw[i] = pchunk_word(la0 + i); bw[i] = pchunk_word(lb0 + i); }
+        const bool x_border_warp = __any_sync(0xffffffffu, has_out && !x_interior);
+        uint8_t* obase = p.bin + (int64_t)blockIdx.z * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
+        nbar_arrive(BAR_FREE0, nthr);  // both prefix buffers start free
+        nbar_arrive(BAR_FREE0 + 1, nthr);
+        for (int k = it.nwarm; k < it.n; ++k) {
+            const int y = it.ya + (k - it.nwarm);
+            const int s = k % NS;
+            const int b = (k - it.nwarm) & 1;
+            nbar_sync(BAR_READY0 + b, nthr);
+            mbar_wait(&full[s], (k / NS) & 1);  // (complete; makes the staged rows visible)
+            const uint8_t* stage = ring + (size_t)s * 3 * p.NC;
+            const uint32_t* sPS = sm + (2 * b) * NCp;
+            const uint32_t* sPQ = sm + (2 * b + 1) * NCp;
+            if (has_out) {
+                const bool y_interior = (y - p.r >= 0) && (y + p.r <= p.H - 1);
+                uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
+                const int ny = min(y + p.r, p.H - 1) - max(y - p.r, 0) + 1;
+                const uint8_t* fsm = stage + 2 * p.NC + VO * to;
+                uint32_t ow[VO / 4];
+                bool unc;
+                if (y_interior && !x_border_warp)
+                    unc = row_outputs<VO, RXM4, METHOD, false>(sPS, sPQ, aw, bw, fsm, ow, xo, p.cols,
+                                                              ny, p.r, p);
+                else
+                    unc = row_outputs<VO, RXM4, METHOD, true>(sPS, sPQ, aw, bw, fsm, ow, xo, p.cols,
+                                                             ny, p.r, p);
+                if (out_full) {
+#pragma unroll
+                    for (int q = 0; q < VO / 16; ++q)
+                        __stcs(reinterpret_cast<uint4*>(orow + xo + 16 * q),
+                               make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < VO; ++j) {
+                        const int x = xo + j;
+                        if (x >= 0 && x < p.cols) orow[x] = (uint8_t)(ow[j >> 2] >> (8 * (j & 3)));
+                    }
+                }
+                if (__builtin_expect(unc, 0))
+                    fix_uncertain<METHOD>(sPS, sPQ, alpha + VO * to, alpha + 2 * p.rx + 1 + VO * to,
+                                          in0 + (int64_t)y * p.pitch, orow, xo, VO, p.cols, ny, p.r,
+                                          p.N, p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            nbar_arrive(BAR_FREE0 + b, nthr);
+        }
     }
 }
 
@@ -694,6 +1049,64 @@ static int slide_v() {
     return v;
 }
 
+
+// ---- warp-specialized launcher
+template <int VO, int RXM4, int METHOD>
+static cudaError_t ws_run(dim3 grid, int nt, size_t smem, const SlideParams& p, cudaStream_t st,
+                          int* occ) {
+    static size_t granted = 48 * 1024;
+    auto kern = ws_kernel<VO, RXM4, METHOD>;
+    if (smem > granted) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        granted = smem;
+    }
+    if (occ) {
+        static int c_nt[16], c_occ[16];
+        static size_t c_smem[16];
+        static int nc = 0;
+        for (int i = 0; i < nc; ++i)
+            if (c_nt[i] == nt && c_smem[i] == smem) { *occ = c_occ[i]; return cudaSuccess; }
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nt, smem) != cudaSuccess)
+            blocks = 1;
+        *occ = std::max(blocks, 1);
+        if (nc < 16) { c_nt[nc] = nt; c_smem[nc] = smem; c_occ[nc] = *occ; ++nc; }
+        return cudaSuccess;
+    }
+    kern<<<grid, nt, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int VO>
+static cudaError_t ws_dispatch_vo(int m, bool sv, dim3 grid, int nt, size_t smem,
+                                  const SlideParams& p, cudaStream_t st, int* occ) {
+    switch (m) {
+        case 0: return sv ? ws_run<VO, 0, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ) : ws_run<VO, 0, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
+        case 1: return sv ? ws_run<VO, 1, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ) : ws_run<VO, 1, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
+        case 2: return sv ? ws_run<VO, 2, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ) : ws_run<VO, 2, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
+        default: return sv ? ws_run<VO, 3, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ) : ws_run<VO, 3, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
+    }
+}
+
+// outputs per output thread: 32 (16 measured slower on B200 and is not exposed)
+static int ws_vo() { return 32; }
+
+static cudaError_t ws_dispatch(int m, bool sv, dim3 grid, int nt, size_t smem, const SlideParams& p,
+                               cudaStream_t st, int* occ) {
+    return ws_dispatch_vo<32>(m, sv, grid, nt, smem, p, st, occ);
+}
+
+static int use_ws() {
+    static int v = -1;
+    if (v < 0) {
+        const char* env = getenv("DTB_WS");
+        v = env ? atoi(env) : DTB_WS_DEFAULT;
+    }
+    return v;
+}
+
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
     slide_constants(p);
     const int V = slide_v();
@@ -715,6 +1128,27 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         }
     }
     if (best_w == 0) return cudaErrorInvalidValue;  // window too wide for 8 warps (caller checks)
+    // warp-specialized kernel when the strip has >= 2 column warps (measured: C4 0.624 vs 0.656
+    // ms; single-column-warp strips such as C3's are faster on the classic kernel)
+    const int ws_mode = use_ws();
+    if (V == 32 && (ws_mode == 1 || (ws_mode == 2 && best_w >= 2))) {
+        p.ncw = best_w;
+        p.now = (best_tw + 32 * ws_vo() - 1) / (32 * ws_vo());
+        p.NC = 1024 * best_w;
+        p.TW = best_tw;
+        const int nt = 32 * (p.ncw + p.now);
+        const size_t smem = ws_smem_bytes(p.NC);
+        const int m = p.rx & 3;
+        const bool sv = p.method == DTB_METHOD_SAUVOLA;
+        int occ = 1;
+        ws_dispatch(m, sv, dim3(), nt, smem, p, st, &occ);
+        const int slots = num_sms * occ;
+        int nbands = std::max(1, slots / std::max(1, best_strips * n_images));
+        nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
+        p.TH = (rows_out + nbands - 1) / nbands;
+        dim3 grid(best_strips, (rows_out + p.TH - 1) / p.TH, n_images);
+        return ws_dispatch(m, sv, grid, nt, smem, p, st, nullptr);
+    }
     const int nt = 32 * best_w;
     p.NC = V * nt;
     p.TW = best_tw;

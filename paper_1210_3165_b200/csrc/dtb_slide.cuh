@@ -23,9 +23,12 @@ struct SlideParams {
     float cA, cC, tol; // fp32 fast-path constants (for n = N) and certified tolerance
     float a, c;        // Sauvola: 1-k, k/R; Niblack: 1, k (border constants are rebuilt per n)
     int l2hint;        // 1: evict_last / evict_first L2 policies on the staged row copies
+    int ncw, now;      // warp-specialized kernel: column warps, output warps
 };
 
+#ifndef SLIDE_STAGES
 #define SLIDE_STAGES 4
+#endif
 
 // Words of one padded prefix array (logical 16-byte chunk L stored at chunk L + L/8).
 __host__ __device__ inline int slide_padded_words(int NC) {
@@ -37,6 +40,12 @@ __host__ __device__ inline int slide_padded_words(int NC) {
 // mbarriers, and NS ring stages of (entering, leaving, centre) row segments of NC bytes.
 __host__ __device__ inline size_t slide_smem_bytes(int NC) {
     return sizeof(uint32_t) * (2 * (size_t)slide_padded_words(NC) + 16) +
+           2 * SLIDE_STAGES * sizeof(uint64_t) + (size_t)SLIDE_STAGES * 3 * NC;
+}
+
+// Warp-specialized kernel: two prefix buffers instead of one.
+__host__ __device__ inline size_t ws_smem_bytes(int NC) {
+    return sizeof(uint32_t) * (4 * (size_t)slide_padded_words(NC) + 32) +
            2 * SLIDE_STAGES * sizeof(uint64_t) + (size_t)SLIDE_STAGES * 3 * NC;
 }
 

@@ -1,0 +1,11 @@
+for R in 168 200; do
+  DTB_NVCC_EXTRA="-DDTB_WS_MAXREG=$R" python paper_1210_3165_b200/build.py --force > /dev/null 2>&1
+  for W in 0 1; do
+    echo -n "maxreg=$R ws=$W  "
+    DTB_WS=$W timeout 120 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-e2e | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('c4', d['kernel_ms'])"
+    echo -n "                   "
+    DTB_WS=$W timeout 120 python bench.py --config c3 --steps 20 --warmup 5 --no-cpu-baseline --no-e2e | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('c3', d['kernel_ms'])"
+  done
+done
+python paper_1210_3165_b200/build.py --force > /dev/null 2>&1
+DTB_WS=1 timeout 600 python -m pytest tests/test_fast_path_gpu.py tests/test_parity_gpu.py -m gpu -x -q 2>&1 | tail -2
