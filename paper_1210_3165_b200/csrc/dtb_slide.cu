@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 
 #include "docthresh_b200.h"
 #include "dtb_common.cuh"
@@ -108,6 +109,24 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 
 // padded shared-memory position (in words) of logical chunk L
 __device__ __forceinline__ int pchunk_word(int L) { return 4 * (L + (L >> 3)); }
+
+// DTB_DEBUG_BOUNDS=1: trap on any out-of-range shared-memory index (debug builds; the pool's
+// compute-sanitizer is unavailable, tests/test_fast_path_gpu.py runs once under this build).
+#ifndef DTB_DEBUG_BOUNDS
+#define DTB_DEBUG_BOUNDS 0
+#endif
+#if DTB_DEBUG_BOUNDS
+#define DTB_CHECK(cond)                                                                       \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("DTB_CHECK failed %s:%d block (%d,%d,%d) thread %d\n", __FILE__, __LINE__, \
+                   blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);                           \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define DTB_CHECK(cond) ((void)0)
+#endif
 
 __device__ __forceinline__ float sqrt_ftz(float x) {
     float y;
@@ -213,10 +232,12 @@ __device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t*
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 if (q < 2 || MA) {
+                    DTB_CHECK(aw[2 * g + q] >= 0 && aw[2 * g + q] + 4 <= slide_padded_words(p.NC));
                     const uint4 v = *reinterpret_cast<const uint4*>(sp + aw[2 * g + q]);
                     A[4 * q] = v.x; A[4 * q + 1] = v.y; A[4 * q + 2] = v.z; A[4 * q + 3] = v.w;
                 }
                 if (q < 2 || MB) {
+                    DTB_CHECK(bw[2 * g + q] >= 0 && bw[2 * g + q] + 4 <= slide_padded_words(p.NC));
                     const uint4 v = *reinterpret_cast<const uint4*>(sp + bw[2 * g + q]);
                     B[4 * q] = v.x; B[4 * q + 1] = v.y; B[4 * q + 2] = v.z; B[4 * q + 3] = v.w;
                 }
@@ -557,6 +578,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
                 cbS[h] += cS[c0 + 3]; cbQ[h] += cQ[c0 + 3];
 #endif
                 const int pw = pchunk_word((V / 4) * t + c0 / 4);
+                DTB_CHECK(pw >= 0 && pw + 4 <= NCp);
                 if (!(DTB_DIAG_SKIP & 2)) {
                     *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
                     *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
@@ -862,6 +884,7 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
                     vs.w = cbS[h]; vq.w = cbQ[h];
                     cbS[h] += cS[c0 + 3]; cbQ[h] += cQ[c0 + 3];
                     const int pw = pchunk_word((V / 4) * t + c0 / 4);
+                DTB_CHECK(pw >= 0 && pw + 4 <= NCp);
                     *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
                     *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
                 }
