@@ -76,3 +76,86 @@ def binarize(img, w, method, k, r=128.0):
     else:
         tmap = mean + k * std
     return np.where(img.astype(np.float64) < tmap, 0, 255).astype(np.uint8), tmap
+
+
+def mask_offsets(structure, w):
+    """masks.py:28-64 + 98-114: GS-1..GS-6 / full offsets, row-major (dy outer, dx inner)."""
+    r = w // 2
+
+    def member(dx, dy):
+        cross = dx == 0 or dy == 0
+        xx = dx == dy or dx == -dy
+        ring = max(abs(dx), abs(dy)) == r
+        return {"gs1": cross, "gs2": xx, "gs3": cross or xx, "gs4": dy == 0 or xx,
+                "gs5": ring or (dx == 0 and dy == 0), "gs6": cross or ring,
+                "full": True}[structure]
+
+    return [(dx, dy) for dy in range(-r, r + 1) for dx in range(-r, r + 1) if member(dx, dy)]
+
+
+def sampled_sums(img, offsets):
+    """stats.py:133-147 _accumulate, in exact integers: (S, Q, count) over in-bounds offsets."""
+    img = np.asarray(img, dtype=np.int64)
+    h, w = img.shape
+    S = np.zeros((h, w), np.int64)
+    Q = np.zeros((h, w), np.int64)
+    n = np.zeros((h, w), np.int64)
+    for dx, dy in offsets:
+        y0, y1 = max(0, -dy), min(h, h - dy)
+        x0, x1 = max(0, -dx), min(w, w - dx)
+        if y0 >= y1 or x0 >= x1:
+            continue
+        v = img[y0 + dy:y1 + dy, x0 + dx:x1 + dx]
+        S[y0:y1, x0:x1] += v
+        Q[y0:y1, x0:x1] += v * v
+        n[y0:y1, x0:x1] += 1
+    return S, Q, n
+
+
+def mean_std_sampled(img, structure, w):
+    """stats.py:150-163 (fp64 sums of integers are exact, so integer sums give the same bits)."""
+    S, Q, n = sampled_sums(img, mask_offsets(structure, w))
+    mean, std = finish(S, Q, n)
+    return mean, std, n
+
+
+def threshold_map(mean, std, method, k, r=128.0):
+    """threshold.py:143-147 / metrics.py:126-129."""
+    if method == "sauvola":
+        return mean * (1.0 + k * (std / r - 1.0))
+    return mean + k * std
+
+
+def evaluate_counts(pred, gt):
+    """metrics.py:52-61 -> (tp, tn, fp, fn, recall, precision, f_measure)."""
+    pf = np.asarray(pred) == 0
+    gf = np.asarray(gt) == 0
+    tp = int(np.count_nonzero(pf & gf))
+    fp = int(np.count_nonzero(pf & ~gf))
+    fn = int(np.count_nonzero(~pf & gf))
+    tn = pf.size - tp - fp - fn
+    recall = tp / (tp + fn) if tp + fn else 0.0
+    precision = tp / (tp + fp) if tp + fp else 0.0
+    fm = 2 * recall * precision / (recall + precision) if recall + precision else 0.0
+    return tp, tn, fp, fn, recall, precision, fm
+
+
+def sweep(img, gt, method, engine, mask, w_grid, k_grid, r=128.0):
+    """metrics.py:105-136 for sauvola/niblack: ([(w, k, fm)], best) with the strict-> tie rule."""
+    img = np.asarray(img, dtype=np.uint8)
+    ws = sorted(int(w) for w in w_grid)
+    ks = sorted(float(k) for k in k_grid)
+    cells, best = [], None
+    for w in ws:
+        if engine in ("naive", "integral") or mask == "full":
+            mean, std = finish(*window_sums_integral(img, w))
+        else:
+            mean, std, _ = mean_std_sampled(img, mask, w)
+        for k in ks:
+            tmap = threshold_map(mean, std, method, k, r)
+            pred = np.where(img.astype(np.float64) < tmap, 0, 255)
+            cell = (w, k, evaluate_counts(pred, gt)[6])
+            cells.append(cell)
+            if best is None or cell[2] > best[2]:
+                best = cell
+    return cells, best

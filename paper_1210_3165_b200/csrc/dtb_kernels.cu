@@ -32,7 +32,7 @@ namespace dtb {
 
 static thread_local char g_err[512] = "";
 
-static int fail(int code, const char* fmt, ...) {
+int fail(int code, const char* fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
@@ -40,7 +40,7 @@ static int fail(int code, const char* fmt, ...) {
     return code;
 }
 
-static int cuda_fail(cudaError_t e, const char* where) {
+int cuda_fail(cudaError_t e, const char* where) {
     return fail(DTB_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
@@ -340,7 +340,7 @@ __global__ void sat_cols_kernel(int rows, int cols, int64_t* s, int64_t* sq) {
 
 static int g_num_sms = 0;
 
-static int num_sms() {
+int num_sms() {
     if (g_num_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);

@@ -51,3 +51,23 @@ def load_json(name):
 def sha(a) -> str:
     import hashlib
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def load_sampled():
+    """sampled.npz (make_golden.make_sampled): GS-mask cases with reference output hashes."""
+    import json
+    z = np.load(os.path.join(GOLDEN, "sampled.npz"))
+    meta = json.loads(str(z["meta"]))
+    return [dict(m, img=z[f"img{i}"], idx=i) for i, m in enumerate(meta)]
+
+
+def load_metrics():
+    """metrics.npz (make_golden.make_metrics): evaluate() pairs and sweep() grids."""
+    import json
+    z = np.load(os.path.join(GOLDEN, "metrics.npz"))
+    meta = json.loads(str(z["meta"]))
+    ev = [dict(pred=z[f"pred{i}"], gt=z[f"gt{i}"], expect=e, idx=i)
+          for i, e in enumerate(meta["evaluate"])]
+    pages = [(z[f"page{p}"], z[f"page_gt{p}"]) for p in range(2)]
+    sw = [dict(s, idx=i) for i, s in enumerate(meta["sweep"])]
+    return ev, pages, sw

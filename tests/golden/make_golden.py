@@ -10,6 +10,11 @@ Writes (all committed; nothing here reads /root/reference at test time):
 * to_gray.json   -- sha256 of the reference to_gray over all 2^24 RGB triples
                     (r-major order), plus every triple where it differs from
                     exact integer half-up rounding (the fp64 tie cases).
+* sampled.npz    -- GS-mask ("sampled" engine) cases: input, structure, W and sha256 of
+                    the reference's mean_std_sampled mean/std/count and of
+                    binarize(engine="sampled") binary/tmap.
+* metrics.npz    -- evaluate() counts/ratios on random bi-level pairs and full sweep()
+                    grids (cells + best) on gen_synthetic pages (§8 row f2).
 * configs.json   -- per BASELINE config: sha256 of the generated input and of
                     the reference's binary output (and tmap for c1/c5), at
                     FULL size.  c4 takes ~90 s and ~21 GB RSS.
@@ -163,16 +168,103 @@ def make_configs(skip_big: bool):
     run("c4/w127", workloads.c4_image(), 127, cfg["c4"])
 
 
+STRUCTS = ("gs1", "gs2", "gs3", "gs4", "gs5", "gs6")
+
+
+def make_sampled(rng):
+    out, meta = {}, []
+    shapes = [(1, 1), (1, 17), (17, 1), (5, 5), (24, 37), (40, 33), (64, 64), (9, 130)]
+    i = 0
+    for st in STRUCTS:
+        for (h, w) in shapes:
+            for win in (3, 7, 21):
+                img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+                if i % 5 == 0:  # document-like: mostly light, few dark strokes
+                    img = np.where(rng.random((h, w)) < 0.1, rng.integers(0, 60, (h, w)),
+                                   rng.integers(170, 230, (h, w))).astype(np.uint8)
+                mask = ref.make_mask(st, win)
+                mean, std, count = ref.mean_std_sampled(img, mask)
+                method = "sauvola" if i % 2 == 0 else "niblack"
+                k = 0.34 if method == "sauvola" else -0.2
+                kw = {"k_sauvola": k} if method == "sauvola" else {"k_niblack": k}
+                b, t = ref.binarize(img, ref.BinarizationParams(
+                    method=method, engine="sampled", mask=st, window=win, **kw))
+                out[f"img{i}"] = img
+                meta.append({"structure": st, "win": win, "method": method, "k": k,
+                             "mean": sha(mean), "std": sha(std),
+                             "count": sha(count.astype(np.int64)),
+                             "binary": sha(b), "tmap": sha(t)})
+                i += 1
+    # the reference's default parameters (sauvola / sampled / gs3 / W=21) on a larger page
+    img = workloads.doc_gray(300, 410, 7, 40)
+    b, t = ref.binarize(img)
+    out[f"img{i}"] = img
+    meta.append({"structure": "gs3", "win": 21, "method": "sauvola", "k": 0.34,
+                 "binary": sha(b), "tmap": sha(t), "default_params": True})
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(os.path.join(HERE, "sampled.npz"), **out)
+    print(f"sampled.npz: {len(meta)} cases")
+
+
+def make_metrics(rng):
+    from docthresh.bench import SyntheticSpec, gen_synthetic
+    out, meta = {}, {"evaluate": [], "sweep": []}
+    for i in range(12):
+        h, w = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+        fr = float(rng.choice([0.0, 0.05, 0.3, 0.9, 1.0]))
+        pred = np.where(rng.random((h, w)) < fr, 0, 255).astype(np.uint8)
+        gt = np.where(rng.random((h, w)) < 0.3, 0, 255).astype(np.uint8)
+        if i % 4 == 3:
+            gt = pred.copy()
+        rep = ref.evaluate(pred, gt)
+        out[f"pred{i}"], out[f"gt{i}"] = pred, gt
+        meta["evaluate"].append([rep.tp, rep.tn, rep.fp, rep.fn, rep.recall, rep.precision,
+                                 rep.f_measure])
+    pages = [gen_synthetic(), gen_synthetic(SyntheticSpec(width=300, height=180, noise_seed=3,
+                                                          noise_amplitude=20))]
+    for p, (img, gt) in enumerate(pages):
+        out[f"page{p}"], out[f"page_gt{p}"] = img, gt
+    cases = [
+        (0, "sauvola", "sampled", "gs3", None, None, 128.0),
+        (0, "sauvola", "naive", "gs3", [21], [0.34], 128.0),
+        (0, "sauvola", "sampled", "gs2", [11, 21], [0.2, 0.4], 128.0),
+        (0, "niblack", "integral", "gs3", [11, 21], [-0.5, -0.2], 128.0),
+        (0, "otsu", "sampled", "gs3", [3, 5], [0.1], 128.0),
+        (1, "sauvola", "integral", "gs3", [41, 3, 15], [0.5, 0.05, 0.2, 0.34], 100.0),
+        (1, "niblack", "sampled", "gs5", [7, 31], [-0.3, 0.0, 0.2], 128.0),
+        (1, "sauvola", "sampled", "gs6", [9], [0.1, 0.3], 64.0),
+        (1, "sauvola", "sampled", "full", [9, 13], [0.25], 128.0),
+    ]
+    for page, method, eng, mask, wg, kg, r in cases:
+        img, gt = pages[page]
+        kw = {}
+        if wg is not None:
+            kw = {"w_grid": wg, "k_grid": kg}
+        res = ref.sweep(img, gt, method=method, engine=eng, mask=mask, r=r, **kw)
+        meta["sweep"].append({"page": page, "method": method, "engine": eng, "mask": mask,
+                              "w_grid": wg, "k_grid": kg, "r": r,
+                              "cells": [[c.w, c.k, c.f_measure] for c in res.cells],
+                              "best": [res.best.w, res.best.k, res.best.f_measure],
+                              "csv": res.to_csv()})
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
+    print(f"metrics.npz: {len(meta['evaluate'])} evaluate, {len(meta['sweep'])} sweep cases")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-big", action="store_true")
-    ap.add_argument("--only", choices=["small", "to_gray", "configs"])
+    ap.add_argument("--only", choices=["small", "to_gray", "configs", "sampled", "metrics"])
     a = ap.parse_args()
     rng = np.random.default_rng(20261019)
     if a.only in (None, "small"):
         make_small(rng)
     if a.only in (None, "to_gray"):
         make_to_gray()
+    if a.only in (None, "sampled"):
+        make_sampled(np.random.default_rng(20261020))
+    if a.only in (None, "metrics"):
+        make_metrics(np.random.default_rng(20261021))
     if a.only in (None, "configs"):
         make_configs(a.skip_big)
 
