@@ -1,0 +1,360 @@
+// dtb_gs.cu -- O(1)-per-pixel GS-mask ("sampled" engine) statistics and binarization
+// (SURVEY.md §8 row f1).
+//
+// Reference: /root/reference/pkg/src/docthresh
+//   masks.py:28-64    GS-1..GS-6 membership predicates over a W x W window (r = W // 2)
+//   masks.py:98-114   make_mask: the offsets, row-major
+//   stats.py:133-163  _accumulate + mean_std_sampled: sums over the IN-BOUNDS offsets,
+//                     count = number of in-bounds offsets, then _finish_arrays
+//   threshold.py:121-148 binarize(engine="sampled") = that + the Sauvola/Niblack epilogue
+//
+// Every GS structure is a union of straight segments through the window:
+//   R0  centre row  (dx in [-r, r], dy = 0)         C0  centre column (dx = 0)
+//   D+  main diagonal (dx = dy)                       D-  anti-diagonal (dx = -dy)
+//   RT/RB ring top / bottom rows (dy = -r / +r, full width)
+//   RL/RR ring left / right columns (dx = -r / +r, dy in [-r+1, r-1])
+//   gs1 = R0 + C0 - c            gs2 = D+ + D- - c          gs3 = R0 + C0 + D+ + D- - 3c
+//   gs4 = R0 + D+ + D- - 2c      gs5 = RT + RB + RL + RR + c
+//   gs6 = R0 + C0 - c + RT + RB + RL + RR - {(0,-r), (0,r), (-r,0), (r,0)}
+// (c = the centre pixel; the subtractions remove the points two segments share).
+//
+// One CTA owns a TY x TX output tile.  The tile plus an r-pixel halo is staged once in
+// shared memory as bytes, zero outside the image, so a segment's in-bounds sum is just its
+// sum over the padded tile.  Each segment family is then a 1-D sliding sum along its
+// direction: a thread owns 16 consecutive outputs of one line, pays 2r+1 loads to start
+// the line and 2 per further output -- O(1) per pixel in W.  Row and diagonal families
+// accumulate into a shared (S, Q) array; column families accumulate in the registers of
+// the thread that finishes those pixels.  Counts are closed-form clipped segment lengths.
+// The epilogue is the reference's fp64 sequence (finish_exact / threshold_exact), so the
+// output is bit-identical.  Sums are exact uint32 (|mask| * 255^2 < 2^32 for every W this
+// kernel accepts).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "docthresh_b200.h"
+#include "dtb_common.cuh"
+
+namespace dtb {
+
+constexpr int GS_TY = 32;     // output rows per tile
+constexpr int GS_TX = 128;    // output columns per tile
+constexpr int GS_NT = 256;    // threads per CTA
+constexpr int GS_SEG = 16;    // outputs per thread per segment family
+constexpr int GS_ACC = GS_TX + 1;  // uint2 row stride of the accumulator (bank-conflict pad)
+static_assert(GS_TY * GS_TX == GS_NT * GS_SEG, "one 16-output run per thread");
+
+struct GsParams {
+    const uint8_t* in;
+    int64_t pitch;
+    int rows, cols, r;
+    int pw;  // shared-memory pitch of the padded tile (bytes, == 4 mod 8)
+    double* mean;
+    double* sd;
+    int32_t* cnt;
+    uint8_t* bin;
+    int64_t bin_pitch;
+    double* tmap;
+    int method;
+    double k, rr;
+};
+
+__device__ __forceinline__ int clip_len(int a, int b, int n) {
+    return max(0, min(b, n - 1) - max(a, 0) + 1);
+}
+
+// Row family at tile row offset oy (0 = R0, -r = RT, +r = RB).  Thread: line i = lane,
+// outputs j in [16*warp, +16).  Writes (FIRST) or adds into acc.
+template <bool FIRST>
+__device__ __forceinline__ void gs_rows(const uint8_t* tile, int pw, uint2* acc, int r, int oy) {
+    const int i = threadIdx.x & 31, j0 = (threadIdx.x >> 5) * GS_SEG;
+    const uint8_t* row = tile + (i + r + oy) * pw;
+    uint32_t s = 0, q = 0;
+    for (int c = j0; c <= j0 + 2 * r; ++c) {
+        const uint32_t v = row[c];
+        s += v;
+        q += v * v;
+    }
+    uint2* a = acc + i * GS_ACC + j0;
+#pragma unroll
+    for (int u = 0; u < GS_SEG; ++u) {
+        if (u) {
+            const uint32_t e = row[j0 + u + 2 * r], l = row[j0 + u - 1];
+            s += e - l;
+            q += e * e - l * l;
+        }
+        if (FIRST) {
+            a[u] = make_uint2(s, q);
+        } else {
+            uint2 o = a[u];
+            o.x += s;
+            o.y += q;
+            a[u] = o;
+        }
+    }
+}
+
+// Diagonal families.  DIR = +1: D+ (tile points (i+d, j+d), d in [0, 2r]); DIR = -1: D-
+// (points (i+2r-d, j+d)).  Thread: column j0 = tid & 127, rows [i0, i0+16); output u is
+// (i0+u, (j0 + DIR*u) mod 128), so consecutive outputs of a thread lie on one line except
+// where the column wraps -- there the line restarts from edge[] (precomputed start sums).
+template <int DIR, bool FIRST>
+__device__ __forceinline__ void gs_diag(const uint8_t* tile, int pw, uint2* acc, const uint2* edge,
+                                        int r) {
+    const int j0 = threadIdx.x & (GS_TX - 1), i0 = (threadIdx.x >> 7) * GS_SEG;
+    uint32_t s = 0, q = 0;
+    for (int d = 0; d <= 2 * r; ++d) {
+        const uint32_t v = DIR > 0 ? tile[(i0 + d) * pw + j0 + d] : tile[(i0 + 2 * r - d) * pw + j0 + d];
+        s += v;
+        q += v * v;
+    }
+#pragma unroll
+    for (int u = 0; u < GS_SEG; ++u) {
+        const int i = i0 + u, j = (j0 + DIR * u) & (GS_TX - 1);
+        if (u) {
+            if (j == (DIR > 0 ? 0 : GS_TX - 1)) {
+                const uint2 e = edge[i];
+                s = e.x;
+                q = e.y;
+            } else {
+                uint32_t e, l;
+                if (DIR > 0) {
+                    e = tile[(i + 2 * r) * pw + j + 2 * r];
+                    l = tile[(i - 1) * pw + j - 1];
+                } else {
+                    e = tile[(i + 2 * r) * pw + j];
+                    l = tile[(i - 1) * pw + j + 2 * r + 1];
+                }
+                s += e - l;
+                q += e * e - l * l;
+            }
+        }
+        uint2* a = acc + i * GS_ACC + j;
+        if (FIRST) {
+            *a = make_uint2(s, q);
+        } else {
+            uint2 o = *a;
+            o.x += s;
+            o.y += q;
+            *a = o;
+        }
+    }
+}
+
+// Column family at tile column offset ox with half-length h (C0: ox = 0, h = r; RL/RR:
+// ox = -r/+r, h = r-1).  Thread: column j, rows [i0, i0+16) -- the finishing layout, so the
+// sums stay in registers.
+__device__ __forceinline__ void gs_cols(const uint8_t* tile, int pw, int r, int ox, int h, int j,
+                                        int i0, uint32_t (&vs)[GS_SEG], uint32_t (&vq)[GS_SEG]) {
+    const uint8_t* col = tile + j + r + ox;
+    uint32_t s = 0, q = 0;
+    for (int d = i0 + r - h; d <= i0 + r + h; ++d) {
+        const uint32_t v = col[d * pw];
+        s += v;
+        q += v * v;
+    }
+#pragma unroll
+    for (int u = 0; u < GS_SEG; ++u) {
+        if (u) {
+            const uint32_t e = col[(i0 + u + r + h) * pw], l = col[(i0 + u - 1 + r - h) * pw];
+            s += e - l;
+            q += e * e - l * l;
+        }
+        vs[u] += s;
+        vq[u] += q;
+    }
+}
+
+template <int GS>
+__global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
+    extern __shared__ __align__(16) uint8_t gs_smem[];
+    const int r = p.r, pw = p.pw;
+    const int PR = GS_TY + 2 * r, PC = GS_TX + 2 * r;
+    uint2* acc = reinterpret_cast<uint2*>(gs_smem);
+    uint2* edge_p = acc + GS_TY * GS_ACC;
+    uint2* edge_m = edge_p + GS_TY;
+    uint8_t* tile = reinterpret_cast<uint8_t*>(edge_m + GS_TY);
+
+    const int ty0 = blockIdx.y * GS_TY, tx0 = blockIdx.x * GS_TX;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // Stage the padded tile (zero outside the image).
+    for (int pr = warp; pr < PR; pr += GS_NT / 32) {
+        const int gy = ty0 - r + pr;
+        const bool rowok = gy >= 0 && gy < p.rows;
+        const uint8_t* src = p.in + (int64_t)gy * p.pitch;
+        for (int pc = lane; pc < PC; pc += 32) {
+            const int gx = tx0 - r + pc;
+            tile[pr * pw + pc] = (rowok && gx >= 0 && gx < p.cols) ? __ldg(src + gx) : 0;
+        }
+    }
+    __syncthreads();
+
+    constexpr bool HAS_DIAG = GS == 2 || GS == 3 || GS == 4;
+    constexpr bool HAS_R0 = GS == 1 || GS == 3 || GS == 4 || GS == 6;
+    constexpr bool HAS_RING = GS == 5 || GS == 6;
+    if (HAS_DIAG && threadIdx.x < 2 * GS_TY) {
+        // Line-start sums where a thread's diagonal run wraps: D+ at column 0, D- at 127.
+        const int i = threadIdx.x & (GS_TY - 1);
+        uint32_t s = 0, q = 0;
+        if (threadIdx.x < GS_TY) {
+            for (int d = 0; d <= 2 * r; ++d) {
+                const uint32_t v = tile[(i + d) * pw + d];
+                s += v;
+                q += v * v;
+            }
+            edge_p[i] = make_uint2(s, q);
+        } else {
+            for (int d = 0; d <= 2 * r; ++d) {
+                const uint32_t v = tile[(i + 2 * r - d) * pw + GS_TX - 1 + d];
+                s += v;
+                q += v * v;
+            }
+            edge_m[i] = make_uint2(s, q);
+        }
+    }
+    if (HAS_R0) gs_rows<true>(tile, pw, acc, r, 0);
+    if (HAS_RING) {
+        if (HAS_R0) gs_rows<false>(tile, pw, acc, r, -r);
+        else gs_rows<true>(tile, pw, acc, r, -r);
+        gs_rows<false>(tile, pw, acc, r, r);
+    }
+    if (HAS_DIAG) {
+        __syncthreads();  // edge sums visible
+        if (HAS_R0) gs_diag<1, false>(tile, pw, acc, edge_p, r);
+        else gs_diag<1, true>(tile, pw, acc, edge_p, r);
+        __syncthreads();  // D+ and D- runs of different threads touch the same acc cells
+        gs_diag<-1, false>(tile, pw, acc, edge_m, r);
+    }
+    const int j = threadIdx.x & (GS_TX - 1), i0 = (threadIdx.x >> 7) * GS_SEG;
+    uint32_t vs[GS_SEG], vq[GS_SEG];
+#pragma unroll
+    for (int u = 0; u < GS_SEG; ++u) vs[u] = vq[u] = 0;
+    if (GS == 1 || GS == 3 || GS == 6) gs_cols(tile, pw, r, 0, r, j, i0, vs, vq);
+    if (HAS_RING) {
+        gs_cols(tile, pw, r, -r, r - 1, j, i0, vs, vq);
+        gs_cols(tile, pw, r, r, r - 1, j, i0, vs, vq);
+    }
+    __syncthreads();  // row / diagonal accumulators complete
+    // Fold the column families into this thread's own accumulator cells.
+#pragma unroll
+    for (int u = 0; u < GS_SEG; ++u) {
+        uint2* a = acc + (i0 + u) * GS_ACC + j;
+        uint2 o = *a;
+        o.x += vs[u];
+        o.y += vq[u];
+        *a = o;
+    }
+
+    const int x = tx0 + j;
+    if (x >= p.cols) return;
+#pragma unroll 1
+    for (int u = 0; u < GS_SEG; ++u) {
+        const int i = i0 + u, y = ty0 + i;
+        if (y >= p.rows) break;
+        const uint2 a = acc[i * GS_ACC + j];
+        uint32_t S = a.x, Q = a.y;
+        const uint32_t f = tile[(i + r) * pw + j + r];
+        const int rows = p.rows, cols = p.cols;
+        const int cx = clip_len(x - r, x + r, cols), cy = clip_len(y - r, y + r, rows);
+        int n = 0;
+        if (GS == 1 || GS == 3 || GS == 6) n += cx + cy;  // R0 + C0
+        if (GS == 4) n += cx;
+        if (HAS_DIAG) {
+            const int dp = min(r, min(cols - 1 - x, rows - 1 - y)) - max(-r, max(-x, -y)) + 1;
+            const int dm = min(r, min(cols - 1 - x, y)) - max(-r, max(-x, y - rows + 1)) + 1;
+            n += dp + dm;
+        }
+        if (HAS_RING) {
+            const int ch = clip_len(y - r + 1, y + r - 1, rows);
+            n += (y - r >= 0 ? cx : 0) + (y + r < rows ? cx : 0) + (x - r >= 0 ? ch : 0) +
+                 (x + r < cols ? ch : 0);
+        }
+        // Points shared by two segments (out-of-image pixels are 0 in the tile).
+        if (GS == 1 || GS == 2) { S -= f; Q -= f * f; n -= 1; }
+        if (GS == 3) { S -= 3 * f; Q -= 3 * f * f; n -= 3; }
+        if (GS == 4) { S -= 2 * f; Q -= 2 * f * f; n -= 2; }
+        if (GS == 5) { S += f; Q += f * f; n += 1; }
+        if (GS == 6) {
+            S -= f;
+            Q -= f * f;
+            n -= 1;
+            const uint32_t t0 = tile[i * pw + j + r], t1 = tile[(i + 2 * r) * pw + j + r];
+            const uint32_t t2 = tile[(i + r) * pw + j], t3 = tile[(i + r) * pw + j + 2 * r];
+            S -= t0 + t1 + t2 + t3;
+            Q -= t0 * t0 + t1 * t1 + t2 * t2 + t3 * t3;
+            n -= (y - r >= 0) + (y + r < rows) + (x - r >= 0) + (x + r < cols);
+        }
+        double mean, sd;
+        finish_exact((double)S, (double)Q, (double)n, mean, sd);
+        const int64_t idx = (int64_t)y * cols + x;
+        if (p.mean) p.mean[idx] = mean;
+        if (p.sd) p.sd[idx] = sd;
+        if (p.cnt) p.cnt[idx] = n;
+        if (p.bin) {
+            const double t = threshold_exact(mean, sd, p.method, p.k, p.rr);
+            p.bin[(int64_t)y * p.bin_pitch + x] = ((double)f < t) ? 0 : 255;
+            if (p.tmap) p.tmap[idx] = t;
+        }
+    }
+}
+
+static int gs_pitch(int r) {
+    const int pc = GS_TX + 2 * r;
+    return ((pc + 7) & ~7) + 4;  // == 4 (mod 8): consecutive tile rows hit distinct banks
+}
+
+size_t gs_smem_bytes(int r) {
+    return sizeof(uint2) * (GS_TY * GS_ACC + 2 * GS_TY) + (size_t)(GS_TY + 2 * r) * gs_pitch(r);
+}
+
+}  // namespace dtb
+
+using namespace dtb;
+
+extern "C" {
+
+int dtb_gs_stats(const uint8_t* gray, int64_t pitch, int32_t rows, int32_t cols, int32_t structure,
+                 int32_t win, double* mean, double* std_, int32_t* count, uint8_t* binary,
+                 int64_t binary_pitch, double* tmap, int32_t method, double k, double r,
+                 void* stream) {
+    if (!gray) return fail(DTB_E_INVALID, "null pointer");
+    if (rows <= 0 || cols <= 0) return fail(DTB_E_INVALID, "image is empty");
+    if (win < 3 || win % 2 == 0) return fail(DTB_E_INVALID, "window: must be an odd integer >= 3, got %d", win);
+    if (structure < DTB_GS1 || structure > DTB_GS6)
+        return fail(DTB_E_INVALID, "structure: expected DTB_GS1..DTB_GS6, got %d", structure);
+    if (!binary && !mean && !std_ && !count) return fail(DTB_E_INVALID, "no output requested");
+    if (binary && method != DTB_METHOD_SAUVOLA && method != DTB_METHOD_NIBLACK)
+        return fail(DTB_E_INVALID, "method: unknown code %d", method);
+    if (pitch < cols || (binary && binary_pitch < cols))
+        return fail(DTB_E_INVALID, "pitch smaller than the row width");
+    const int rad = win / 2;
+    const size_t smem = gs_smem_bytes(rad);
+    if (smem > DTB_GS_MAX_SMEM)
+        return fail(DTB_E_UNSUPPORTED, "window %d too large for the tiled GS kernel", win);
+    GsParams p{gray, pitch, rows, cols, rad, gs_pitch(rad), mean, std_, count, binary,
+               binary_pitch, tmap, method, k, r};
+    const dim3 grid((cols + GS_TX - 1) / GS_TX, (rows + GS_TY - 1) / GS_TY);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+#define DTB_GS_LAUNCH(G)                                                                      \
+    case G: {                                                                                 \
+        e = cudaFuncSetAttribute(gs_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                 (int)smem);                                                  \
+        if (e == cudaSuccess) gs_kernel<G><<<grid, GS_NT, smem, st>>>(p);                     \
+        break;                                                                                \
+    }
+    switch (structure) {
+        DTB_GS_LAUNCH(1)
+        DTB_GS_LAUNCH(2)
+        DTB_GS_LAUNCH(3)
+        DTB_GS_LAUNCH(4)
+        DTB_GS_LAUNCH(5)
+        DTB_GS_LAUNCH(6)
+    }
+#undef DTB_GS_LAUNCH
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? DTB_OK : cuda_fail(e, "gs_kernel launch");
+}
+
+}  // extern "C"

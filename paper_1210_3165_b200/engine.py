@@ -165,6 +165,44 @@ def sampled(gray, offsets, method: str | None = None, k: float = 0.0, r: float =
     return out, tmap
 
 
+GS_CODES = {"gs1": 1, "gs2": 2, "gs3": 3, "gs4": 4, "gs5": 5, "gs6": 6}
+
+
+def gs(gray, structure: str, win: int, method: str | None = None, k: float = 0.0,
+       r: float = 128.0, want_tmap: bool = True, stream=None):
+    """GS-mask statistics / binarization in O(1) per pixel (dtb_gs_stats).
+
+    Same results and return convention as ``sampled`` with make_mask(structure, win)'s
+    offsets.  Windows whose tile does not fit in shared memory go to ``sampled``.
+    """
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    L = _lib.lib()
+    code = GS_CODES[structure]
+    if method is None:
+        mean = torch.empty((h, w), dtype=torch.float64, device=g.device)
+        std = torch.empty_like(mean)
+        cnt = torch.empty((h, w), dtype=torch.int32, device=g.device)
+        rc = L.dtb_gs_stats(g.data_ptr(), g.stride(0), h, w, code, int(win), mean.data_ptr(),
+                            std.data_ptr(), cnt.data_ptr(), None, 0, None, 0, 0.0, 1.0,
+                            _stream(stream))
+        res = {"mean": mean, "std": std, "count": cnt}
+    else:
+        out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
+        tmap = torch.empty((h, w), dtype=torch.float64, device=g.device) if want_tmap else None
+        rc = L.dtb_gs_stats(g.data_ptr(), g.stride(0), h, w, code, int(win), None, None, None,
+                            out.data_ptr(), out.stride(0),
+                            tmap.data_ptr() if tmap is not None else None,
+                            METHOD_CODES[method], float(k), float(r), _stream(stream))
+        res = (out, tmap)
+    if rc == _lib.DTB_E_UNSUPPORTED:
+        from .masks import make_mask
+        return sampled(g, make_mask(structure, win).offsets, method, k, r, want_tmap, stream)
+    _lib.check(rc, "dtb_gs_stats")
+    return res
+
+
 def to_gray(rgb, stream=None):
     torch = torch_mod()
     t = to_device(rgb, ndim=3, what="rgb")

@@ -154,7 +154,8 @@ def _stats(dev, engine_name: str, mask: str, w: int):
     if engine_name in ("naive", "integral") or mask == "full":
         d = engine.window_stats(dev, w, want=("mean", "std"))
     else:
-        d = engine.sampled(dev, make_mask(mask, w).offsets)
+        m = make_mask(mask, w)
+        d = engine.gs(dev, m.structure, m.window)
     return d["mean"], d["std"]
 
 

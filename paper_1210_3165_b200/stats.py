@@ -76,6 +76,8 @@ def mean_std_sampled(img, mask: SamplingMask):
     dev = engine.to_device(img)
     if mask.structure == "full":
         return _out(engine.window_stats(dev, mask.window, want=("mean", "std", "count")), host)
+    if mask.structure in engine.GS_CODES:
+        return _out(engine.gs(dev, mask.structure, mask.window), host)
     return _out(engine.sampled(dev, mask.offsets), host)
 
 

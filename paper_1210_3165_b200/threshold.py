@@ -177,9 +177,9 @@ def binarize(img, params: BinarizationParams = BinarizationParams(), *, return_t
         binary, tmap = engine.binarize(dev, params.window, params.method, params.k, params.r,
                                        want_tmap=return_tmap)
     else:
-        offs = make_mask(params.mask, params.window).offsets
-        binary, tmap = engine.sampled(dev, offs, params.method, params.k, params.r,
-                                      want_tmap=return_tmap)
+        mask = make_mask(params.mask, params.window)
+        binary, tmap = engine.gs(dev, mask.structure, mask.window, params.method, params.k,
+                                 params.r, want_tmap=return_tmap)
     if host:
         return _host(binary, src, out), _host(tmap, src)
     return binary, tmap
