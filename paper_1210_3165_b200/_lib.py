@@ -35,7 +35,7 @@ SIGNATURES = {
     "dtb_window_stats": [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p,
                          _c_p],
     "dtb_sampled_stats": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i32, _c_p, _c_p, _c_p, _c_p,
-                          _c_i64, _c_i32, _c_f64, _c_f64, _c_p],
+                          _c_p, _c_i32, _c_f64, _c_f64, _c_p],
     "dtb_histogram": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
     "dtb_integral_tables": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p],
     "dtb_apply_global": [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_p],

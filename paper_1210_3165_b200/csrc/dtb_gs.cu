@@ -58,6 +58,9 @@ struct GsParams {
     double* tmap;
     int method;
     double k, rr;
+    int nmask;      // |mask| = the count of every unclipped window
+    int fast;       // binary only (no tmap / stats): certified fp32 decision
+    FastConsts fc;  // for the interior count |mask|
 };
 
 __device__ __forceinline__ int clip_len(int a, int b, int n) {
@@ -166,6 +169,46 @@ __device__ __forceinline__ void gs_cols(const uint8_t* tile, int pw, int r, int 
     }
 }
 
+// Remove the points two segments share from (S, Q) (out-of-image pixels are 0 in the tile).
+template <int GS>
+__device__ __forceinline__ void gs_overlaps(const uint8_t* tile, int pw, int r, int i, int j,
+                                            uint32_t f, uint32_t& S, uint32_t& Q) {
+    if (GS == 1 || GS == 2) { S -= f; Q -= f * f; }
+    if (GS == 3) { S -= 3 * f; Q -= 3 * f * f; }
+    if (GS == 4) { S -= 2 * f; Q -= 2 * f * f; }
+    if (GS == 5) { S += f; Q += f * f; }
+    if (GS == 6) {
+        const uint32_t t0 = tile[i * pw + j + r], t1 = tile[(i + 2 * r) * pw + j + r];
+        const uint32_t t2 = tile[(i + r) * pw + j], t3 = tile[(i + r) * pw + j + 2 * r];
+        S -= f + t0 + t1 + t2 + t3;
+        Q -= f * f + t0 * t0 + t1 * t1 + t2 * t2 + t3 * t3;
+    }
+}
+
+// Interior tile, binary only: every count is |mask|, so the per-launch fp32 constants apply
+// to all 16 pixels; uncertain pixels replay the reference fp64 sequence (exact_white).
+template <int GS, int METHOD>
+__device__ __forceinline__ void gs_fast_interior(const GsParams& p, const uint8_t* tile,
+                                                 const uint2* acc, const uint32_t (&vs)[GS_SEG],
+                                                 const uint32_t (&vq)[GS_SEG], int i0, int j,
+                                                 int tx0, int ty0) {
+    const int r = p.r, pw = p.pw;
+    uint8_t* out = p.bin + (int64_t)(ty0 + i0) * p.bin_pitch + tx0 + j;
+#pragma unroll
+    for (int u = 0; u < GS_SEG; ++u) {
+        const int i = i0 + u;
+        const uint2 a = acc[i * GS_ACC + j];
+        uint32_t S = a.x + vs[u], Q = a.y + vq[u];
+        const uint32_t f = tile[(i + r) * pw + j + r];
+        gs_overlaps<GS>(tile, pw, r, i, j, f, S, Q);
+        const float d = fast_diff<METHOD, false>(S, Q, f, p.fc.N, p.fc.cA, p.fc.cC, p.fc.a, p.fc.c);
+        const uint32_t white = fabsf(d) >= p.fc.tol
+                                   ? (d < 0.f ? 0u : 255u)
+                                   : exact_white(S, Q, (double)p.fc.N, f, METHOD, p.k, p.rr);
+        out[(int64_t)u * p.bin_pitch] = (uint8_t)white;
+    }
+}
+
 template <int GS>
 __global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
     extern __shared__ __align__(16) uint8_t gs_smem[];
@@ -178,14 +221,34 @@ __global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
 
     const int ty0 = blockIdx.y * GS_TY, tx0 = blockIdx.x * GS_TX;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // Interior tile: every window of every output is unclipped (count = |mask|), and the
+    // staged rows are followed by at least one more image row (the word loads below may run
+    // up to 7 bytes past a staged row's end).
+    const bool interior = ty0 >= r && ty0 + GS_TY + r < p.rows && tx0 >= r &&
+                          tx0 + GS_TX + r <= p.cols;
     // Stage the padded tile (zero outside the image).
-    for (int pr = warp; pr < PR; pr += GS_NT / 32) {
-        const int gy = ty0 - r + pr;
-        const bool rowok = gy >= 0 && gy < p.rows;
-        const uint8_t* src = p.in + (int64_t)gy * p.pitch;
-        for (int pc = lane; pc < PC; pc += 32) {
-            const int gx = tx0 - r + pc;
-            tile[pr * pw + pc] = (rowok && gx >= 0 && gx < p.cols) ? __ldg(src + gx) : 0;
+    if (interior) {
+        // aligned 4-byte loads, realigned with a funnel shift, 4-byte shared stores
+        const int nw = (PC + 3) >> 2;
+        for (int pr = warp; pr < PR; pr += GS_NT / 32) {
+            const uintptr_t ad = reinterpret_cast<uintptr_t>(p.in + (int64_t)(ty0 - r + pr) * p.pitch +
+                                                             (tx0 - r));
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(ad & ~(uintptr_t)3);
+            const uint32_t sh = (uint32_t)(ad & 3) * 8u;
+            for (int kw = lane; kw < nw; kw += 32) {
+                const uint32_t lo = __ldg(w + kw), hi = __ldg(w + kw + 1);
+                *reinterpret_cast<uint32_t*>(tile + pr * pw + 4 * kw) = __funnelshift_r(lo, hi, sh);
+            }
+        }
+    } else {
+        for (int pr = warp; pr < PR; pr += GS_NT / 32) {
+            const int gy = ty0 - r + pr;
+            const bool rowok = gy >= 0 && gy < p.rows;
+            const uint8_t* src = p.in + (int64_t)gy * p.pitch;
+            for (int pc = lane; pc < PC; pc += 32) {
+                const int gx = tx0 - r + pc;
+                tile[pr * pw + pc] = (rowok && gx >= 0 && gx < p.cols) ? __ldg(src + gx) : 0;
+            }
         }
     }
     __syncthreads();
@@ -236,6 +299,13 @@ __global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
         gs_cols(tile, pw, r, r, r - 1, j, i0, vs, vq);
     }
     __syncthreads();  // row / diagonal accumulators complete
+    if (p.fast && interior) {  // the common case: unclipped windows, binary output only
+        if (p.method == DTB_METHOD_SAUVOLA)
+            gs_fast_interior<GS, DTB_METHOD_SAUVOLA>(p, tile, acc, vs, vq, i0, j, tx0, ty0);
+        else
+            gs_fast_interior<GS, DTB_METHOD_NIBLACK>(p, tile, acc, vs, vq, i0, j, tx0, ty0);
+        return;
+    }
     // Fold the column families into this thread's own accumulator cells.
 #pragma unroll
     for (int u = 0; u < GS_SEG; ++u) {
@@ -256,34 +326,44 @@ __global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
         uint32_t S = a.x, Q = a.y;
         const uint32_t f = tile[(i + r) * pw + j + r];
         const int rows = p.rows, cols = p.cols;
-        const int cx = clip_len(x - r, x + r, cols), cy = clip_len(y - r, y + r, rows);
-        int n = 0;
-        if (GS == 1 || GS == 3 || GS == 6) n += cx + cy;  // R0 + C0
-        if (GS == 4) n += cx;
-        if (HAS_DIAG) {
-            const int dp = min(r, min(cols - 1 - x, rows - 1 - y)) - max(-r, max(-x, -y)) + 1;
-            const int dm = min(r, min(cols - 1 - x, y)) - max(-r, max(-x, y - rows + 1)) + 1;
-            n += dp + dm;
+        gs_overlaps<GS>(tile, pw, r, i, j, f, S, Q);
+        int n = p.nmask;
+        if (!interior) {  // closed-form clipped segment lengths
+            const int cx = clip_len(x - r, x + r, cols), cy = clip_len(y - r, y + r, rows);
+            n = 0;
+            if (GS == 1 || GS == 3 || GS == 6) n += cx + cy;  // R0 + C0
+            if (GS == 4) n += cx;
+            if (HAS_DIAG) {
+                const int dp = min(r, min(cols - 1 - x, rows - 1 - y)) - max(-r, max(-x, -y)) + 1;
+                const int dm = min(r, min(cols - 1 - x, y)) - max(-r, max(-x, y - rows + 1)) + 1;
+                n += dp + dm;
+            }
+            if (HAS_RING) {
+                const int ch = clip_len(y - r + 1, y + r - 1, rows);
+                n += (y - r >= 0 ? cx : 0) + (y + r < rows ? cx : 0) + (x - r >= 0 ? ch : 0) +
+                     (x + r < cols ? ch : 0);
+            }
+            if (GS == 1 || GS == 2) n -= 1;
+            if (GS == 3) n -= 3;
+            if (GS == 4) n -= 2;
+            if (GS == 5) n += 1;
+            if (GS == 6)
+                n -= 1 + (y - r >= 0) + (y + r < rows) + (x - r >= 0) + (x + r < cols);
         }
-        if (HAS_RING) {
-            const int ch = clip_len(y - r + 1, y + r - 1, rows);
-            n += (y - r >= 0 ? cx : 0) + (y + r < rows ? cx : 0) + (x - r >= 0 ? ch : 0) +
-                 (x + r < cols ? ch : 0);
-        }
-        // Points shared by two segments (out-of-image pixels are 0 in the tile).
-        if (GS == 1 || GS == 2) { S -= f; Q -= f * f; n -= 1; }
-        if (GS == 3) { S -= 3 * f; Q -= 3 * f * f; n -= 3; }
-        if (GS == 4) { S -= 2 * f; Q -= 2 * f * f; n -= 2; }
-        if (GS == 5) { S += f; Q += f * f; n += 1; }
-        if (GS == 6) {
-            S -= f;
-            Q -= f * f;
-            n -= 1;
-            const uint32_t t0 = tile[i * pw + j + r], t1 = tile[(i + 2 * r) * pw + j + r];
-            const uint32_t t2 = tile[(i + r) * pw + j], t3 = tile[(i + r) * pw + j + 2 * r];
-            S -= t0 + t1 + t2 + t3;
-            Q -= t0 * t0 + t1 * t1 + t2 * t2 + t3 * t3;
-            n -= (y - r >= 0) + (y + r < rows) + (x - r >= 0) + (x + r < cols);
+        if (p.fast) {
+            // binary only: certified fp32 decision, fp64 replay for the uncertain pixels
+            const uint32_t un = (uint32_t)n;
+            float d;
+            if (p.method == DTB_METHOD_SAUVOLA)
+                d = un == p.fc.N ? fast_diff<DTB_METHOD_SAUVOLA, false>(S, Q, f, un, p.fc.cA, p.fc.cC, p.fc.a, p.fc.c)
+                                 : fast_diff<DTB_METHOD_SAUVOLA, true>(S, Q, f, un, p.fc.cA, p.fc.cC, p.fc.a, p.fc.c);
+            else
+                d = un == p.fc.N ? fast_diff<DTB_METHOD_NIBLACK, false>(S, Q, f, un, p.fc.cA, p.fc.cC, p.fc.a, p.fc.c)
+                                 : fast_diff<DTB_METHOD_NIBLACK, true>(S, Q, f, un, p.fc.cA, p.fc.cC, p.fc.a, p.fc.c);
+            const uint32_t white = fabsf(d) >= p.fc.tol ? (d < 0.f ? 0u : 255u)
+                                                        : exact_white(S, Q, (double)n, f, p.method, p.k, p.rr);
+            p.bin[(int64_t)y * p.bin_pitch + x] = (uint8_t)white;
+            continue;
         }
         double mean, sd;
         finish_exact((double)S, (double)Q, (double)n, mean, sd);
@@ -333,7 +413,14 @@ int dtb_gs_stats(const uint8_t* gray, int64_t pitch, int32_t rows, int32_t cols,
     if (smem > DTB_GS_MAX_SMEM)
         return fail(DTB_E_UNSUPPORTED, "window %d too large for the tiled GS kernel", win);
     GsParams p{gray, pitch, rows, cols, rad, gs_pitch(rad), mean, std_, count, binary,
-               binary_pitch, tmap, method, k, r};
+               binary_pitch, tmap, method, k, r, 0, 0, FastConsts{}};
+    static const int mul[7] = {0, 2, 2, 4, 3, 4, 6};  // |mask| = mul*W - sub (masks.py:5-12)
+    static const int sub[7] = {0, 1, 1, 3, 2, 3, 9};
+    p.nmask = mul[structure] * win - sub[structure];
+    if (binary && !tmap && !mean && !std_ && !count) {
+        p.fast = 1;
+        p.fc = fast_constants(method, k, r, (double)p.nmask);
+    }
     const dim3 grid((cols + GS_TX - 1) / GS_TX, (rows + GS_TY - 1) / GS_TY);
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;

@@ -128,54 +128,7 @@ __device__ __forceinline__ int pchunk_word(int L) { return 4 * (L + (L >> 3)); }
 #define DTB_CHECK(cond) ((void)0)
 #endif
 
-__device__ __forceinline__ float sqrt_ftz(float x) {
-    float y;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-__device__ __forceinline__ float rcp_ftz(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// f - t_fp32 for one pixel.  cA/cC: per-launch constants for n = N (interior); at borders
-// (BORDER) they are rebuilt from the pixel's own count n with an fp32 reciprocal.
-template <int METHOD, bool BORDER>
-__device__ __forceinline__ float fast_diff(uint32_t S, uint32_t Q, uint32_t f, uint32_t n,
-                                           float cA, float cC, float a, float c) {
-    const uint64_t D = (uint64_t)n * Q - (uint64_t)S * S;  // exact, >= 0
-#if DTB_D_SPLIT
-    // D < 2^49: hi*2^32 + lo with two full-rate I2FP conversions and one FFMA (rel. err 2^-23)
-    const float Df = __fmaf_rn((float)(uint32_t)(D >> 32), 4294967296.0f, (float)(uint32_t)D);
-#else
-    const float Df = (float)D;  // I2F.U64 (XU pipe)
-#endif
-    const float sD = sqrt_ftz(Df);
-    const float Sf = (float)S;
-    if (BORDER) {
-        const float rn = rcp_ftz((float)n);
-        if (METHOD == DTB_METHOD_SAUVOLA) {
-            cA = a * rn;           // (1-k)/n
-            cC = c * (rn * rn);    // k/(R n^2)
-        } else {
-            cA = rn;               // 1/n
-            cC = c * rn;           // k/n
-        }
-    }
-    if (METHOD == DTB_METHOD_SAUVOLA) return __fmaf_rn(-Sf, __fmaf_rn(sD, cC, cA), (float)f);
-    return __fmaf_rn(-cC, sD, __fmaf_rn(-cA, Sf, (float)f));
-}
-
-// Reference fp64 decision for one pixel (threshold.py:143-147 over stats.py:50-54).
-__device__ __noinline__ uint32_t exact_white(uint32_t S, uint32_t Q, double n, uint32_t f,
-                                             int method, double k, double rr) {
-    double mean, sd;
-    finish_exact((double)S, (double)Q, n, mean, sd);
-    const double t = threshold_exact(mean, sd, method, k, rr);
-    return ((double)f < t) ? 0u : 0xFFu;
-}
+// sqrt_ftz, rcp_ftz, fast_diff, exact_white: dtb_common.cuh
 
 // Rare path, out of line: re-decide this thread's 32 pixels, the uncertain ones (|f - t32| < tol)
 // with the reference fp64 sequence.  S/Q are read back from the shared prefix (valid until the next
@@ -975,27 +928,14 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
 void slide_constants(SlideParams& p) {
     const char* env = getenv("DTB_L2HINT");
     p.l2hint = env ? atoi(env) : 1;
-    const double W = 2.0 * p.r + 1.0, N = W * W;
-    p.N = (uint32_t)N;
-    const double sd_err = 6.6e-6, rel = 1.5e-6;
-    double e_ref, e_fast;
-    if (p.method == DTB_METHOD_SAUVOLA) {
-        const double kr = p.k / p.rr;
-        p.a = (float)(1.0 - p.k);
-        p.c = (float)kr;
-        p.cA = (float)((1.0 - p.k) / N);
-        p.cC = (float)(kr / (N * N));
-        e_ref = 255.0 * kr * sd_err;
-        e_fast = 255.0 * (1.0 + std::fabs(p.k) * (127.5 / p.rr + 1.0)) * rel;
-    } else {
-        p.a = 1.0f;
-        p.c = (float)p.k;
-        p.cA = (float)(1.0 / N);
-        p.cC = (float)(p.k / N);
-        e_ref = std::fabs(p.k) * sd_err;
-        e_fast = (255.0 + std::fabs(p.k) * 127.5) * rel;
-    }
-    p.tol = (float)(2.0 * (e_ref + e_fast) + 1e-6);
+    const double W = 2.0 * p.r + 1.0;
+    const FastConsts fc = fast_constants(p.method, p.k, p.rr, W * W);
+    p.N = fc.N;
+    p.a = fc.a;
+    p.c = fc.c;
+    p.cA = fc.cA;
+    p.cC = fc.cC;
+    p.tol = fc.tol;
 }
 
 // Host-side launch state is cached per instantiation: the dynamic-smem opt-in is raised once to

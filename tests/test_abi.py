@@ -49,6 +49,29 @@ def test_python_signature_table_covers_header():
     assert set(declared_symbols()) == set(_lib.SIGNATURES)
 
 
+def _header_prototypes():
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    protos = {}
+    for m in re.finditer(r"^\s*(?:int|const char \*)\s*(dtb_\w+)\s*\(([^)]*)\)\s*;", text,
+                         re.M | re.S):
+        args = [a.strip() for a in m.group(2).split(",") if a.strip() and a.strip() != "void"]
+        protos[m.group(1)] = args
+    return protos
+
+
+def test_python_signature_types_match_header():
+    """Every ctypes argtype agrees with the C prototype (pointer / int64 / int32 / double)."""
+    want = {"int64_t": ctypes.c_int64, "int32_t": ctypes.c_int32, "double": ctypes.c_double}
+    protos = _header_prototypes()
+    assert set(protos) == set(_lib.SIGNATURES)
+    for name, args in protos.items():
+        got = _lib.SIGNATURES[name]
+        assert len(got) == len(args), name
+        for a, t in zip(args, got):
+            exp = ctypes.c_void_p if "*" in a else want[a.split()[0]]
+            assert t is exp, f"{name}: {a!r} bound as {t}"
+
+
 def test_library_is_sm100a():
     build.build()
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],

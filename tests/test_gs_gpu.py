@@ -65,3 +65,22 @@ def test_gs_huge_window_falls_back_to_gather(rng):
     m, s, n = dt.mean_std_sampled(img, dt.make_mask("gs3", 601))  # tile > shared memory
     om, os_, on = numpy_ref.mean_std_sampled(img, "gs3", 601)
     assert np.array_equal(n, on) and np.array_equal(m, om) and np.array_equal(s, os_)
+
+
+@pytest.mark.parametrize("structure", STRUCTS)
+def test_gs_fast_path_near_ties(rng, structure):
+    """Binary-only (certified fp32) path on images built to put f at or near t."""
+    import torch
+    cases = [(rng.choice([100, 101], (150, 290)).astype(np.uint8), "niblack", 0.0),
+             (rng.choice([0, 255], (150, 290)).astype(np.uint8), "niblack", 0.0),
+             (rng.choice([60, 61, 62], (150, 290)).astype(np.uint8), "sauvola", 0.5),
+             (np.full((150, 290), 77, np.uint8), "sauvola", 0.34),
+             (rng.integers(0, 256, (150, 290)).astype(np.uint8), "niblack", -0.2)]
+    for img, method, k in cases:
+        for win in (3, 9, 21):
+            b, _ = engine.gs(torch.from_numpy(img).cuda(), structure, win, method, k, 128.0,
+                             want_tmap=False)
+            om, os_, _ = numpy_ref.mean_std_sampled(img, structure, win)
+            tm = numpy_ref.threshold_map(om, os_, method, k)
+            want = np.where(img.astype(np.float64) < tm, 0, 255).astype(np.uint8)
+            assert np.array_equal(b.cpu().numpy(), want), (method, k, win)
