@@ -159,3 +159,29 @@ def sweep(img, gt, method, engine, mask, w_grid, k_grid, r=128.0):
             if best is None or cell[2] > best[2]:
                 best = cell
     return cells, best
+
+
+def otsu_threshold(img):
+    """threshold.py:55-88: Otsu T with the strict-> smallest-T tie rule, Python arithmetic."""
+    img = np.asarray(img, dtype=np.uint8)
+    hist = np.bincount(img.ravel(), minlength=256).astype(np.int64)
+    total = int(hist.sum())
+    sum_all = int(np.dot(hist, np.arange(256, dtype=np.int64)))
+    best_t, best_var = -1, -1.0
+    wb = sumb = 0
+    for t in range(256):
+        wb += int(hist[t])
+        sumb += t * int(hist[t])
+        if wb == 0:
+            continue
+        wf = total - wb
+        if wf == 0:
+            break
+        mb = sumb / wb
+        mf = (sum_all - sumb) / wf
+        var = wb * wf * (mb - mf) ** 2
+        if var > best_var:
+            best_var, best_t = var, t
+    if best_t < 0:
+        return int(img.flat[0])
+    return best_t + 1

@@ -41,6 +41,8 @@ SIGNATURES = {
     "dtb_apply_global": [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_p],
     "dtb_gs_stats": [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_i64,
                      _c_p, _c_i32, _c_f64, _c_f64, _c_p],
+    "dtb_otsu": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p],
+    "dtb_apply_global_dev": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p, _c_p],
     "dtb_confusion": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
     "dtb_sweep_counts": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p,
                          _c_i32, _c_i32, _c_f64, _c_p, _c_p],

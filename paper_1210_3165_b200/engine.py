@@ -251,6 +251,34 @@ def apply_global(gray, t: int, stream=None):
     return out
 
 
+def otsu(gray, stream=None):
+    """Device int32 tensor [1] holding the Otsu T (dtb_otsu); no host synchronisation."""
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    hist = torch.empty(256, dtype=torch.int64, device=g.device)
+    t = torch.empty(1, dtype=torch.int32, device=g.device)
+    rc = _lib.lib().dtb_otsu(g.data_ptr(), g.stride(0), h, w, hist.data_ptr(), t.data_ptr(),
+                             _stream(stream))
+    _lib.check(rc, "dtb_otsu")
+    return t
+
+
+def apply_global_dev(gray, t_dev, want_tmap: bool = False, stream=None):
+    """(binary, tmap or None) with T from a device int32 tensor (dtb_apply_global_dev)."""
+    torch = torch_mod()
+    g = to_device(gray)
+    h, w = g.shape
+    out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
+    tmap = torch.empty((h, w), dtype=torch.float64, device=g.device) if want_tmap else None
+    rc = _lib.lib().dtb_apply_global_dev(g.data_ptr(), g.stride(0), h, w, t_dev.data_ptr(),
+                                         out.data_ptr(), out.stride(0),
+                                         tmap.data_ptr() if tmap is not None else None,
+                                         _stream(stream))
+    _lib.check(rc, "dtb_apply_global_dev")
+    return out, tmap
+
+
 def integral_tables(gray, stream=None):
     """(H+1, W+1) int64 summed-area tables of f and f^2 (stats.py:82-91)."""
     torch = torch_mod()

@@ -99,33 +99,9 @@ def _host(t, like=None, out=None):
 
 
 def otsu_threshold(img) -> int:
-    """threshold.py:55-88: histogram on the device, exact 256-step scan on the host."""
+    """threshold.py:55-88: histogram and the exact 256-step scan on the device (dtb_otsu)."""
     dev, _ = _prepare(img)
-    hist = [int(v) for v in engine.histogram(dev).cpu().tolist()]
-    return _otsu_from_hist(hist, lambda: int(dev.reshape(-1)[0].item()))
-
-
-def _otsu_from_hist(hist, first_pixel) -> int:
-    total = sum(hist)
-    sum_all = sum(i * c for i, c in enumerate(hist))
-    best_t, best_var = -1, -1.0
-    wb = sumb = 0
-    for t in range(256):
-        wb += hist[t]
-        sumb += t * hist[t]
-        if wb == 0:
-            continue
-        wf = total - wb
-        if wf == 0:
-            break
-        mb = sumb / wb
-        mf = (sum_all - sumb) / wf
-        var = wb * wf * (mb - mf) ** 2
-        if var > best_var:
-            best_var, best_t = var, t
-    if best_t < 0:
-        return first_pixel()  # single-bin histogram: the image's own value
-    return best_t + 1
+    return int(engine.otsu(dev).item())
 
 
 def apply_global(img, t: int):
@@ -166,13 +142,8 @@ def binarize(img, params: BinarizationParams = BinarizationParams(), *, return_t
     params.validate()
     dev = engine.to_device(img)
     if params.method == "otsu":
-        t = otsu_threshold(dev)
-        binary = engine.apply_global(dev, t)
-        if return_tmap:
-            torch = engine.torch_mod()
-            tmap = torch.full(tuple(dev.shape), float(t), dtype=torch.float64, device=dev.device)
-        else:
-            tmap = None
+        # histogram -> scan -> apply, stream-ordered with T kept on the device
+        binary, tmap = engine.apply_global_dev(dev, engine.otsu(dev), want_tmap=return_tmap)
     elif params.full_window:
         binary, tmap = engine.binarize(dev, params.window, params.method, params.k, params.r,
                                        want_tmap=return_tmap)

@@ -71,3 +71,9 @@ def load_metrics():
     pages = [(z[f"page{p}"], z[f"page_gt{p}"]) for p in range(2)]
     sw = [dict(s, idx=i) for i, s in enumerate(meta["sweep"])]
     return ev, pages, sw
+
+
+def load_otsu():
+    """otsu.npz (make_golden.make_otsu): [(image, reference T)]."""
+    z = np.load(os.path.join(GOLDEN, "otsu.npz"))
+    return [(z[f"img{i}"], int(t)) for i, t in enumerate(z["t"])]

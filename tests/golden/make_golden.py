@@ -15,6 +15,7 @@ Writes (all committed; nothing here reads /root/reference at test time):
                     binarize(engine="sampled") binary/tmap.
 * metrics.npz    -- evaluate() counts/ratios on random bi-level pairs and full sweep()
                     grids (cells + best) on gen_synthetic pages (§8 row f2).
+* otsu.npz       -- images + the reference's otsu_threshold T (§8 row f3).
 * configs.json   -- per BASELINE config: sha256 of the generated input and of
                     the reference's binary output (and tmap for c1/c5), at
                     FULL size.  c4 takes ~90 s and ~21 GB RSS.
@@ -251,10 +252,35 @@ def make_metrics(rng):
     print(f"metrics.npz: {len(meta['evaluate'])} evaluate, {len(meta['sweep'])} sweep cases")
 
 
+def make_otsu(rng):
+    """otsu.npz: images and the reference's otsu_threshold (threshold.py:55-88) for each."""
+    out, ts = {}, []
+    imgs = [np.full((4, 7), 77, np.uint8), np.array([[0, 255]], np.uint8),
+            np.array([[10] * 50 + [200] * 50], np.uint8), np.zeros((1, 1), np.uint8)]
+    for _ in range(10):
+        h, w = int(rng.integers(1, 200)), int(rng.integers(1, 200))
+        imgs.append(rng.integers(0, 256, (h, w)).astype(np.uint8))
+    for _ in range(6):  # bimodal pages, the case Otsu is for
+        h, w = int(rng.integers(50, 300)), int(rng.integers(50, 300))
+        lo, hi = int(rng.integers(10, 90)), int(rng.integers(150, 240))
+        a = np.where(rng.random((h, w)) < rng.uniform(0.05, 0.5), lo, hi)
+        imgs.append(np.clip(a + rng.normal(0, rng.uniform(1, 30), (h, w)), 0, 255).astype(np.uint8))
+    imgs.append(workloads.doc_gray(700, 500, 11, 300))
+    for _ in range(4):  # few-level images: many exact variance ties
+        vals = rng.choice(256, int(rng.integers(2, 5)), replace=False)
+        imgs.append(rng.choice(vals, (int(rng.integers(3, 60)), int(rng.integers(3, 60)))).astype(np.uint8))
+    for i, img in enumerate(imgs):
+        out[f"img{i}"] = img
+        ts.append(int(ref.otsu_threshold(img)))
+    out["t"] = np.array(ts, np.int32)
+    np.savez_compressed(os.path.join(HERE, "otsu.npz"), **out)
+    print(f"otsu.npz: {len(ts)} images")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-big", action="store_true")
-    ap.add_argument("--only", choices=["small", "to_gray", "configs", "sampled", "metrics"])
+    ap.add_argument("--only", choices=["small", "to_gray", "configs", "sampled", "metrics", "otsu"])
     a = ap.parse_args()
     rng = np.random.default_rng(20261019)
     if a.only in (None, "small"):
@@ -265,6 +291,8 @@ def main():
         make_sampled(np.random.default_rng(20261020))
     if a.only in (None, "metrics"):
         make_metrics(np.random.default_rng(20261021))
+    if a.only in (None, "otsu"):
+        make_otsu(np.random.default_rng(20261022))
     if a.only in (None, "configs"):
         make_configs(a.skip_big)
 

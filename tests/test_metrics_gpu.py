@@ -161,3 +161,26 @@ def test_sampled_engine_matches_reference(case):
     b, t = dt.binarize(img, p)
     assert sha(b) == case["binary"]
     assert sha(t) == case["tmap"]
+
+
+def test_otsu_device_scan_matches_reference():
+    """§8 row f3: device histogram + fp64 scan == the reference's T on its own images."""
+    from conftest import load_otsu
+    for img, t in load_otsu():
+        assert dt.otsu_threshold(img) == t
+        b, tm = dt.binarize(img, dt.BinarizationParams(method="otsu"))
+        assert np.array_equal(b, np.where(img < t, 0, 255).astype(np.uint8))
+        assert tm.dtype == np.float64 and np.all(tm == float(t))
+
+
+def test_otsu_large_and_strided(rng):
+    import torch
+    from oracle import numpy_ref
+    img = rng.integers(0, 256, (2049, 3001)).astype(np.uint8)
+    img[:1000] = np.clip(img[:1000] // 4, 0, 255)
+    assert dt.otsu_threshold(img) == numpy_ref.otsu_threshold(img)
+    dev = torch.from_numpy(img).cuda()[3:, 5:]  # unaligned -> scalar histogram path
+    assert dt.otsu_threshold(dev) == numpy_ref.otsu_threshold(img[3:, 5:])
+    b, t = dt.binarize(dev, dt.BinarizationParams(method="otsu"), return_tmap=False)
+    T = numpy_ref.otsu_threshold(img[3:, 5:])
+    assert t is None and torch.equal(b.cpu(), torch.from_numpy(np.where(img[3:, 5:] < T, 0, 255).astype(np.uint8)))

@@ -50,3 +50,9 @@ def test_sweep_oracle_matches_reference(case):
                                   case["k_grid"] or DEFAULT_K_GRID, case["r"])
     assert [list(c) for c in cells] == case["cells"]
     assert list(best) == case["best"]
+
+
+def test_otsu_oracle_matches_reference():
+    from conftest import load_otsu
+    for img, t in load_otsu():
+        assert numpy_ref.otsu_threshold(img) == t
