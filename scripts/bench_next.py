@@ -83,7 +83,33 @@ def main():
     sweep_s = time.perf_counter() - t0
     pred, _ = engine.gs(img, "gs3", 21, "sauvola", 0.34, 128.0, want_tmap=False)
     ev_ms = timed(lambda: dt.evaluate(pred, gt), a.reps)
+    # f4: PNM page pipeline, 12 A4/300dpi RGB pages (C2 shape, P6 files), reference-CLI
+    # default params (sauvola / sampled gs3 / W=21); files in a temp dir, page cache warm.
+    import tempfile
+    from paper_1210_3165_b200 import pipeline
+    rgb = workloads.c2_rgb()
+    h, w = rgb.shape[:2]
+    data = b"P6\n%d %d\n255\n" % (w, h) + rgb.tobytes()
+    pipe = {}
+    with tempfile.TemporaryDirectory() as td:
+        pairs = []
+        for i in range(12):
+            src = os.path.join(td, f"p{i}.ppm")
+            with open(src, "wb") as fh:
+                fh.write(data)
+            pairs.append((src, os.path.join(td, f"o{i}.pgm")))
+        for slots in (1, 2, 3):
+            pipeline.binarize_files(pairs[:2], slots=slots)  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st = pipeline.binarize_files(pairs, slots=slots)
+            torch.cuda.synchronize()
+            dt_s = time.perf_counter() - t0
+            pipe[f"slots{slots}"] = {"pages_per_s": round(st.pages / dt_s, 2),
+                                     "mpx_per_s": round(st.pixels / dt_s / 1e6, 1),
+                                     "file_mb_per_s": round((st.bytes_in + st.bytes_out) / dt_s / 1e6, 1)}
     out = {"gpu": torch.cuda.get_device_name(0), "page": list(img.shape),
+           "pipeline_c2_pages": pipe,
            "l2": "flushed (512 MiB memset) before every rep", "gs": rows,
            "sweep_default_grid_s": round(sweep_s, 4), "sweep_best": list(res.best),
            "evaluate_ms_incl_host_sync": round(ev_ms, 4)}
