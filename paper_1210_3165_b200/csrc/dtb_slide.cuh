@@ -24,6 +24,7 @@ struct SlideParams {
     float a, c;        // Sauvola: 1-k, k/R; Niblack: 1, k (border constants are rebuilt per n)
     int l2hint;        // 1: evict_last / evict_first L2 policies on the staged row copies
     int ncw, now;      // warp-specialized kernel: column warps, output warps
+    int role_div;      // ws: swap the two roles' warp slots in every other group of role_div CTAs (0 = never)
 };
 
 #ifndef SLIDE_STAGES
