@@ -7,11 +7,13 @@
 
 Workload (default): BASELINE config 4 -- a 16384x16384 synthetic gray page,
 Sauvola W=127 k=0.34 R=128, split in row bands across ranks with the 63-row
-halos exchanged point-to-point (NCCL send/recv over NVLink) every step.
+halos read in place from the neighbouring GPUs' HBM over NVLink (CUDA IPC mappings,
+fused into the kernel's row staging; ``--halo nccl`` copies them with NCCL send/recv
+every step instead).
 ``--scaling weak`` (default): every rank owns one full 16384x16384 band of a
 (16384*N)-row page, so per-GPU work is fixed; ``strong`` splits the one
-16384x16384 page N ways.  One step = halo exchange + one pass of the fused
-sliding-sum binarization kernel over the rank's band.
+16384x16384 page N ways.  One step = one pass of the fused sliding-sum
+binarization kernel over the rank's band (plus the NCCL halo copy with --halo nccl).
 
 Prints ONE JSON line (rank 0).  ``value`` is whole-job Mpixel/s with inputs
 resident in HBM, timed with CUDA events (max over ranks); ``e2e`` is the
@@ -50,6 +52,9 @@ def parse():
     ap.add_argument("--config", choices=["c4", "c3", "c5", "c2", "c1"], default="c4")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--window", type=int, default=None, help="override W (c5 sweep point)")
+    ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
+                    help="row-band halos: read in place from the neighbours' HBM (CUDA IPC, "
+                         "fused into the kernel's row staging) or copied with NCCL send/recv")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -149,7 +154,7 @@ def workload(cfg_name, world, rank, scaling, window):
                     method=cfg.method, k=cfg.k, r=cfg.r, px_rank=(y1 - y0) * Wd,
                     desc=(f"{cfg_name}: {H}x{Wd} gray page(s), {cfg.method} W={win} k={cfg.k} "
                           f"R={cfg.r}; {'weak' if scaling == 'weak' else 'strong'} row-band "
-                          f"split over {world} GPU(s), {r}-row halos via NCCL P2P"),
+                          f"split over {world} GPU(s), {r}-row halos"),
                     shape=[rows, Wd])
     if cfg_name == "c3":
         n_total = 64 * (world if scaling == "weak" else 1)
@@ -198,8 +203,18 @@ def run_ours(a):
         outs = [torch.empty_like(band) for _ in range(nrot)]
         r = w["win"] // 2
         ha, hz = D.halo_bounds(w["rows"], w["y0"], w["y1"], r)
+        use_p2p = (world > 1 and a.halo == "p2p" and
+                   all(D.p2p_possible(w["rows"], world, q, r) for q in range(world)))
         halo_bufs = [torch.empty((hz - ha,) + tuple(band.shape[1:]), dtype=torch.uint8,
-                                 device=dev) for _ in range(nrot)] if world > 1 else None
+                                 device=dev) for _ in range(nrot)] if world > 1 and not use_p2p else None
+        # p2p: map the neighbours' bands once (CUDA IPC); each step's kernel then reads the
+        # halo rows in place over NVLink -- no exchange step.  Bands are constant after setup.
+        peers = [D.PeerHalos(bands[j], w["rows"], r) for j in range(nrot)] if use_p2p else None
+        if use_p2p:
+            peers[0].barrier()
+        w["halo"] = ("none (1 GPU)" if world == 1 else
+                     "read in place from the neighbours' HBM over NVLink (CUDA IPC), fused into "
+                     "the kernel's row staging" if use_p2p else "NCCL send/recv copy per step")
         launches_per_step = 1
 
         def kernel(i):
@@ -211,6 +226,13 @@ def run_ours(a):
 
         def step(i, ev=None):
             j = i % nrot
+            if use_p2p:
+                if ev is not None:
+                    ev[0].record(stream)
+                peers[j].binarize(w["win"], w["method"], w["k"], w["r"], out=outs[j], sync=False)
+                if ev is not None:
+                    ev[1].record(stream)
+                return
             buf, a0 = kernel(j)
             if ev is not None:
                 ev[0].record(stream)
@@ -317,6 +339,7 @@ def run_ours(a):
             "config": {"workload": w["desc"], "image": w["shape"], "window": w["win"],
                        "method": w["method"], "k": w["k"], "r": w["r"],
                        "parallelism": f"{'rowband' if w['kind'] == 'rowband' else 'image'}{world}",
+                       **({"halo": w["halo"]} if "halo" in w else {}),
                        "l2": (f"{nrot} rotating input/output buffer sets, "
                               f"{nrot * per_step_bytes / 2**20:.0f} MiB per rank >= 2x L2 "
                               f"({l2 / 2**20:.0f} MiB)")},

@@ -43,6 +43,11 @@ SIGNATURES = {
                      _c_p, _c_i32, _c_f64, _c_f64, _c_p],
     "dtb_otsu": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p],
     "dtb_apply_global_dev": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p, _c_p],
+    "dtb_binarize_segments": [_c_p, _c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
+                              _c_p, _c_i64, _c_i32, _c_i32, _c_f64, _c_f64, _c_p],
+    "dtb_ipc_export": [_c_p, _c_p, _c_p],
+    "dtb_ipc_import": [_c_p, _c_p],
+    "dtb_ipc_close": [_c_p],
     "dtb_confusion": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
     "dtb_sweep_counts": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p,
                          _c_i32, _c_i32, _c_f64, _c_p, _c_p],

@@ -398,7 +398,7 @@ static int launch_strip(StripParams p, int n_images, cudaStream_t st) {
 
 // The fast kernel keeps 32-bit sums: every window sum must stay < 2^32, and the strip
 // (<= 8 warps = 8192 columns) must hold a window plus 32 outputs.
-static bool slide_ok(int r, int cols, int rows, const void* base, int64_t pitch,
+bool slide_ok(int r, int cols, int rows, const void* base, int64_t pitch,
                      int64_t stride) {
     if (const char* env = getenv("DTB_FORCE_V1")) { if (env[0] == '1') return false; }
     // rows are staged with 16-byte bulk copies

@@ -130,6 +130,15 @@ __device__ __forceinline__ int pchunk_word(int L) { return 4 * (L + (L >> 3)); }
 
 // sqrt_ftz, rcp_ftz, fast_diff, exact_white: dtb_common.cuh
 
+// Address of global row g (in0 = the single buffer's row-0 origin).  Segmented inputs pick
+// the segment holding g; the pointer may be a peer GPU's memory (NVLink), which the bulk
+// copies and loads below read in place.
+__device__ __forceinline__ const uint8_t* row_at(const SlideParams& p, const uint8_t* in0, int g) {
+    if (p.nseg == 0) return in0 + (int64_t)g * p.pitch;
+    const int i = g >= p.seg_lo[2] ? 2 : (g >= p.seg_lo[1] ? 1 : 0);
+    return p.seg_ptr[i] + (int64_t)(g - p.seg_lo[i]) * p.seg_pitch[i];
+}
+
 // Rare path, out of line: re-decide this thread's 32 pixels, the uncertain ones (|f - t32| < tol)
 // with the reference fp64 sequence.  S/Q are read back from the shared prefix (valid until the next
 // row's first barrier); corrected bytes are written after the vector stores (program order).
@@ -355,16 +364,16 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             if (gf >= 0) bytes += fb;
             mbar_expect_tx(&full[s], bytes);
             if (ge >= 0 && rowb)
-                bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s], pol_keep);
+                bulk_g2s(E + (c_lo - xc0), row_at(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
             if (go >= 0 && rowb)
-                bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s], pol_drop);
-            if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s], pol_keep);
+                bulk_g2s(O + (c_lo - xc0), row_at(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+            if (gf >= 0 && fb) bulk_g2s(F, row_at(p, in0, gf) + X0, fb, &full[s], pol_keep);
             for (int c = c_hi16; c < c_hi; ++c) {
-                if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
-                if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+                if (ge >= 0) E[c - xc0] = row_at(p, in0, ge)[c];
+                if (go >= 0) O[c - xc0] = row_at(p, in0, go)[c];
             }
             for (int c = f_hi16; c < f_hi; ++c)
-                if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+                if (gf >= 0) F[c - X0] = row_at(p, in0, gf)[c];
         } else if (which == 0) {
             uint32_t bytes = 0;
             if (ge >= 0) bytes += rowb;
@@ -372,18 +381,18 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             if (gf >= 0) bytes += fb;
             mbar_expect_tx(&full[s], bytes);
             if (ge >= 0 && rowb)
-                bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s], pol_keep);
+                bulk_g2s(E + (c_lo - xc0), row_at(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
             for (int c = c_hi16; c < c_hi; ++c) {
-                if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
-                if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+                if (ge >= 0) E[c - xc0] = row_at(p, in0, ge)[c];
+                if (go >= 0) O[c - xc0] = row_at(p, in0, go)[c];
             }
             for (int c = f_hi16; c < f_hi; ++c)
-                if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+                if (gf >= 0) F[c - X0] = row_at(p, in0, gf)[c];
         } else if (which == 1) {
             if (go >= 0 && rowb)
-                bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s], pol_drop);
+                bulk_g2s(O + (c_lo - xc0), row_at(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
         } else {
-            if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s], pol_keep);
+            if (gf >= 0 && fb) bulk_g2s(F, row_at(p, in0, gf) + X0, fb, &full[s], pol_keep);
         }
     };
     const bool producer = DTB_PAR_PRODUCER ? (warp == 0 && lane < 3) : (t == 0);
@@ -591,7 +600,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             }
             if (__builtin_expect(unc, 0))
                 fix_uncertain<METHOD>(sPS, sPQ, alpha + V * t, alpha + 2 * p.rx + 1 + V * t,
-                                      in0 + (int64_t)y * p.pitch, orow, xo, V, p.cols, ny, p.r, p.N,
+                                      row_at(p, in0, y), orow, xo, V, p.cols, ny, p.r, p.N,
                                       p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
         }
         release(k);
@@ -726,16 +735,16 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
         if (gf >= 0) bytes += fb;
         mbar_expect_tx(&full[s], bytes);
         if (ge >= 0 && rowb)
-            bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s], pol_keep);
+            bulk_g2s(E + (c_lo - xc0), row_at(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
         if (go >= 0 && rowb)
-            bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s], pol_drop);
-        if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s], pol_keep);
+            bulk_g2s(O + (c_lo - xc0), row_at(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+        if (gf >= 0 && fb) bulk_g2s(F, row_at(p, in0, gf) + X0, fb, &full[s], pol_keep);
         for (int c = c_hi16; c < c_hi; ++c) {
-            if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
-            if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+            if (ge >= 0) E[c - xc0] = row_at(p, in0, ge)[c];
+            if (go >= 0) O[c - xc0] = row_at(p, in0, go)[c];
         }
         for (int c = f_hi16; c < f_hi; ++c)
-            if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+            if (gf >= 0) F[c - X0] = row_at(p, in0, gf)[c];
     };
 
     if (is_col) {
@@ -916,7 +925,7 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
                 }
                 if (__builtin_expect(unc, 0))
                     fix_uncertain<METHOD>(sPS, sPQ, alpha + VO * to, alpha + 2 * p.rx + 1 + VO * to,
-                                          in0 + (int64_t)y * p.pitch, orow, xo, VO, p.cols, ny, p.r,
+                                          row_at(p, in0, y), orow, xo, VO, p.cols, ny, p.r,
                                           p.N, p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
             }
             __syncwarp();

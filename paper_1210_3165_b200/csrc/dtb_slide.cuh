@@ -24,6 +24,13 @@ struct SlideParams {
     float a, c;        // Sauvola: 1-k, k/R; Niblack: 1, k (border constants are rebuilt per n)
     int l2hint;        // 1: evict_last / evict_first L2 policies on the staged row copies
     int ncw, now;      // warp-specialized kernel: column warps, output warps
+    // Optional segmented input (dtb_binarize_segments): global rows [seg_lo[i], seg_lo[i+1]) live
+    // at seg_ptr[i] with pitch seg_pitch[i] -- e.g. a neighbour GPU's halo rows read in place
+    // over NVLink (peer / IPC pointers).  nseg == 0: the single buffer in/pitch/row0.
+    int nseg;
+    const uint8_t* seg_ptr[3];
+    int64_t seg_pitch[3];
+    int seg_lo[3];
     int role_div;      // ws: swap the two roles' warp slots in every other group of role_div CTAs (0 = never)
 };
 

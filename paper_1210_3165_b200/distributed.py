@@ -11,6 +11,17 @@ strategies, neither needs a reduction collective:
   before the band kernel runs.  Window clipping inside the kernel uses GLOBAL
   row indices, so the stitched bands equal the whole-image result bit for bit.
 
+Two transports for the row-band halos:
+
+* ``"nccl"``: ``exchange_halos`` copies the r boundary rows into a local
+  [halo | band | halo] buffer with batched isend/irecv, then the band kernel runs.
+* ``"p2p"`` (``PeerHalos``): each rank maps its neighbours' band buffers once
+  through CUDA IPC; the band kernel (``dtb_binarize_segments``) then reads the
+  halo rows IN PLACE from the neighbours' HBM over NVLink as part of its own
+  row staging -- the exchange is fused into the compute kernel and there is no
+  copy step to wait for.  Used when every halo row comes from an adjacent
+  rank (bands at least r rows tall) and rows are 16-byte aligned.
+
 The band kernel is injectable (``compute``) so the host-side logic (band
 bounds, halo routing, assembly) is exercised on CPU with world_size 2 under
 gloo; the production call is ``engine.binarize_band`` (libdocthresh_b200).
@@ -86,11 +97,25 @@ def exchange_halos(band: torch.Tensor, rows: int, r: int, group=None,
 
 def binarize_rowbands(band: torch.Tensor, rows: int, win: int, method: str, k: float,
                       r: float, group=None, compute: Callable | None = None,
-                      halo_buf: torch.Tensor | None = None, out: torch.Tensor | None = None):
-    """This rank's binarized rows [y0, y1) of a page split in row bands across the group."""
+                      halo_buf: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                      transport: str = "nccl"):
+    """This rank's binarized rows [y0, y1) of a page split in row bands across the group.
+
+    transport "nccl" copies the halos first (exchange_halos); "p2p" maps the neighbours'
+    bands through CUDA IPC for this one call and reads the halos in place (for repeated
+    steps keep a ``PeerHalos`` instead, which maps once).
+    """
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     y0, y1 = band_bounds(rows, world, rank)
+    if transport == "p2p" and compute is None:
+        ph = PeerHalos(band, rows, win // 2, group)
+        try:
+            res = ph.binarize(win, method, k, r, out=out)
+            ph.barrier()  # neighbours finished reading our band
+            return res
+        finally:
+            ph.close()
     buf, a = exchange_halos(band, rows, win // 2, group, out=halo_buf)
     if compute is None:
         from . import engine
@@ -109,3 +134,94 @@ def binarize_images(stack: torch.Tensor, win: int, method: str, k: float, r: flo
         from . import engine
         return i0, i1, engine.binarize_batch(shard, win, method, k, r, out=out)
     return i0, i1, compute(shard, win, method, k, r)
+
+
+def p2p_segments(rows: int, world: int, rank: int, r: int):
+    """[(src_rank, first row within src's band, n_rows)] stacking global rows [a, z) for rank."""
+    y0, y1 = band_bounds(rows, world, rank)
+    a, z = halo_bounds(rows, y0, y1, r)
+    segs = []
+    if a < y0:
+        n0, _ = band_bounds(rows, world, rank - 1)
+        segs.append((rank - 1, a - n0, y0 - a))
+    segs.append((rank, 0, y1 - y0))
+    if z > y1:
+        segs.append((rank + 1, 0, z - y1))
+    return segs
+
+
+def p2p_possible(rows: int, world: int, rank: int, r: int) -> bool:
+    """True when this rank's halo rows all come from its two adjacent ranks."""
+    return all(src in (rank - 1, rank + 1)
+               for src, dst, _, _ in halo_plan(rows, world, r) if dst == rank)
+
+
+class PeerHalos:
+    """In-place halo reads between ranks (one process per GPU, same node).
+
+    ``PeerHalos(band, rows, r)`` exchanges CUDA IPC handles of every rank's band buffer
+    (a small all_gather_object) and maps the adjacent ranks' buffers.  ``binarize(...)``
+    then runs ``dtb_binarize_segments`` over [upper neighbour's last rows | own band |
+    lower neighbour's first rows].  Contract: every rank's band must be complete before
+    any neighbour's kernel reads it (``binarize(sync=True)`` synchronises the stream and
+    barriers the group first), and a rank must not overwrite its band until its
+    neighbours' kernels are done (call ``barrier()`` after the step).
+    """
+
+    def __init__(self, band: torch.Tensor, rows: int, r: int, group=None):
+        from . import engine
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.rows, self.r = rows, r
+        self.y0, self.y1 = band_bounds(rows, self.world, self.rank)
+        if band.shape[0] != self.y1 - self.y0:
+            raise ValueError(f"rows: band has {band.shape[0]} rows, expected {self.y1 - self.y0}")
+        if not p2p_possible(rows, self.world, self.rank, r):
+            raise ValueError("p2p halos need every halo row on an adjacent rank (bands >= r rows)")
+        self.band = band
+        self.cols = band.shape[1]
+        torch.cuda.current_stream().synchronize()
+        mine = engine.ipc_export(band) + (band.stride(0),)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self.mapped = {}
+        self.addr = {}
+        for nb in (self.rank - 1, self.rank + 1):
+            if 0 <= nb < self.world:
+                h, off, pitch = allh[nb]
+                base = engine.ipc_import(h)
+                self.mapped[nb] = base
+                self.addr[nb] = (base + off, pitch)
+
+    def segments(self):
+        """[(ptr, pitch, rows, cols)] for global rows [a, z) and the first global row a."""
+        a, _ = halo_bounds(self.rows, self.y0, self.y1, self.r)
+        segs = []
+        for src, first, n in p2p_segments(self.rows, self.world, self.rank, self.r):
+            if src == self.rank:
+                ptr, pitch = self.band.data_ptr(), self.band.stride(0)
+            else:  # the neighbour's band, mapped through CUDA IPC (NVLink on a multi-GPU node)
+                ptr, pitch = self.addr[src]
+            segs.append((ptr + first * pitch, pitch, n, self.cols))
+        return segs, a
+
+    def barrier(self):
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
+
+    def binarize(self, win: int, method: str, k: float, r: float, out=None, sync: bool = True):
+        from . import engine
+        if win // 2 != self.r:
+            raise ValueError(f"window: PeerHalos was built for r={self.r}, got W={win}")
+        if sync:
+            self.barrier()
+        segs, a = self.segments()
+        return engine.binarize_segments(segs, a, self.rows, self.y0, self.y1, win, method, k, r,
+                                        out=out)
+
+    def close(self):
+        from . import engine
+        for base in self.mapped.values():
+            engine.ipc_close(base)
+        self.mapped.clear()

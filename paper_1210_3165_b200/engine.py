@@ -103,6 +103,52 @@ def binarize_band(buf, row0_global: int, rows_global: int, out_begin: int, out_e
     return out
 
 
+def binarize_segments(segments, row0_global: int, rows_global: int, out_begin: int,
+                      out_end: int, win: int, method: str, k: float, r: float, out=None,
+                      stream=None):
+    """Binarize global rows [out_begin, out_end) whose input rows are split over up to three
+    buffers (dtb_binarize_segments).  ``segments`` = [(ptr, pitch, rows, cols), ...] with raw
+    device pointers (e.g. a neighbour GPU's band mapped through CUDA IPC) stacked downward
+    from global row ``row0_global``.  Returns the (out_end - out_begin, cols) binary tensor."""
+    import ctypes
+    torch = torch_mod()
+    n = len(segments)
+    cols = segments[0][3]
+    ptrs = (ctypes.c_void_p * 3)(*[sg[0] for sg in segments] + [None] * (3 - n))
+    pitches = (ctypes.c_int64 * 3)(*[sg[1] for sg in segments] + [0] * (3 - n))
+    nrows = (ctypes.c_int32 * 3)(*[sg[2] for sg in segments] + [0] * (3 - n))
+    if out is None:
+        out = torch.empty((out_end - out_begin, cols), dtype=torch.uint8, device="cuda")
+    rc = _lib.lib().dtb_binarize_segments(
+        ptrs, pitches, nrows, n, int(row0_global), int(rows_global), int(cols), int(out_begin),
+        int(out_end), out.data_ptr(), out.stride(0), int(win), METHOD_CODES[method], float(k),
+        float(r), _stream(stream))
+    _lib.check(rc, "dtb_binarize_segments")
+    return out
+
+
+def ipc_export(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t.data_ptr() in it)."""
+    import ctypes
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_int64(0)
+    _lib.check(_lib.lib().dtb_ipc_export(t.data_ptr(), h, ctypes.byref(off)), "dtb_ipc_export")
+    return bytes(h), int(off.value)
+
+
+def ipc_import(handle: bytes) -> int:
+    """Map a peer process's allocation; returns its base device address (close with ipc_close)."""
+    import ctypes
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    base = ctypes.c_void_p(0)
+    _lib.check(_lib.lib().dtb_ipc_import(h, ctypes.byref(base)), "dtb_ipc_import")
+    return int(base.value)
+
+
+def ipc_close(base: int) -> None:
+    _lib.check(_lib.lib().dtb_ipc_close(base), "dtb_ipc_close")
+
+
 def binarize_batch(stack, win: int, method: str, k: float, r: float, out=None, stream=None):
     """(N, H, W) uint8 CUDA stack -> (N, H, W) binary, one launch."""
     torch = torch_mod()

@@ -91,3 +91,33 @@ def test_halo_plan_covers_every_needed_row():
                     assert s0 <= g0 < g1 <= s1
                     got.update(range(g0, g1))
             assert got == set(range(a, y0)) | set(range(y1, z))
+
+
+@pytest.mark.parametrize("rows,world,r", [(100, 4, 10), (64, 2, 31), (1000, 8, 63), (7, 3, 1),
+                                          (50, 5, 10), (16384 * 8, 8, 63)])
+def test_p2p_segments_cover_exactly_the_halo_plan(rows, world, r):
+    """Fused in-place halo reads (PeerHalos) read exactly the rows the NCCL plan would copy."""
+    from paper_1210_3165_b200 import distributed as D
+    for rank in range(world):
+        if not D.p2p_possible(rows, world, rank, r):
+            continue
+        y0, y1 = D.band_bounds(rows, world, rank)
+        a, z = D.halo_bounds(rows, y0, y1, r)
+        segs = D.p2p_segments(rows, world, rank, r)
+        g = a
+        got = []
+        for src, first, n in segs:
+            s0, s1 = D.band_bounds(rows, world, src)
+            assert 0 <= first and first + n <= s1 - s0
+            got.append((src, s0 + first, s0 + first + n))
+            assert s0 + first == g
+            g += n
+        assert g == z
+        want = sorted((src, g0, g1) for src, dst, g0, g1 in D.halo_plan(rows, world, r) if dst == rank)
+        assert sorted(x for x in got if x[0] != rank) == want
+
+
+def test_p2p_possible_rejects_thin_bands():
+    from paper_1210_3165_b200 import distributed as D
+    assert D.p2p_possible(100, 4, 1, 10)
+    assert not D.p2p_possible(100, 8, 1, 20)  # 12-row bands, 20-row halos span two ranks
