@@ -69,7 +69,10 @@ def lib():
             f"{LIB_PATH} is not built; run `python -m paper_1210_3165_b200.build` "
             "(or __graft_entry__.build()). There is no CPU fallback.")
     L = ctypes.CDLL(LIB_PATH)
+    allow_missing = os.environ.get("DTB_AB_ALLOW_MISSING") == "1"  # A/B builds of older sources
     for name, argtypes in SIGNATURES.items():
+        if allow_missing and not hasattr(L, name):
+            continue
         fn = getattr(L, name)
         fn.argtypes = argtypes
         fn.restype = ctypes.c_char_p if name == "dtb_last_error" else ctypes.c_int

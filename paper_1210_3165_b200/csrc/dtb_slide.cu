@@ -133,8 +133,11 @@ __device__ __forceinline__ int pchunk_word(int L) { return 4 * (L + (L >> 3)); }
 // Address of global row g (in0 = the single buffer's row-0 origin).  Segmented inputs pick
 // the segment holding g; the pointer may be a peer GPU's memory (NVLink), which the bulk
 // copies and loads below read in place.
+// SEG is a compile-time kernel variant: the single-buffer kernels keep the plain address
+// arithmetic (a runtime segment test in the producer's path measured 8% slower on C4).
+template <bool SEG>
 __device__ __forceinline__ const uint8_t* row_at(const SlideParams& p, const uint8_t* in0, int g) {
-    if (p.nseg == 0) return in0 + (int64_t)g * p.pitch;
+    if (!SEG) return in0 + (int64_t)g * p.pitch;
     const int i = g >= p.seg_lo[2] ? 2 : (g >= p.seg_lo[1] ? 1 : 0);
     return p.seg_ptr[i] + (int64_t)(g - p.seg_lo[i]) * p.seg_pitch[i];
 }
@@ -281,8 +284,11 @@ struct Items {
 #define DTB_SLIDE_MINB(V) ((V) == 16 ? 2 : 1)
 #endif
 
-template <int V, int RXM4, int METHOD>
+// MX = method code | 4 for the segmented-input variant (dtb_binarize_segments)
+template <int V, int RXM4, int MX>
 __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlideParams p) {
+    constexpr int METHOD = MX & 3;
+    constexpr bool SEG = (MX & 4) != 0;
     constexpr int MA = (4 - RXM4) & 3;
     constexpr int MB = (RXM4 + 1) & 3;
     constexpr int NS = SLIDE_STAGES;
@@ -364,16 +370,16 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             if (gf >= 0) bytes += fb;
             mbar_expect_tx(&full[s], bytes);
             if (ge >= 0 && rowb)
-                bulk_g2s(E + (c_lo - xc0), row_at(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
+                bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
             if (go >= 0 && rowb)
-                bulk_g2s(O + (c_lo - xc0), row_at(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
-            if (gf >= 0 && fb) bulk_g2s(F, row_at(p, in0, gf) + X0, fb, &full[s], pol_keep);
+                bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+            if (gf >= 0 && fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
             for (int c = c_hi16; c < c_hi; ++c) {
-                if (ge >= 0) E[c - xc0] = row_at(p, in0, ge)[c];
-                if (go >= 0) O[c - xc0] = row_at(p, in0, go)[c];
+                if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
+                if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
             }
             for (int c = f_hi16; c < f_hi; ++c)
-                if (gf >= 0) F[c - X0] = row_at(p, in0, gf)[c];
+                if (gf >= 0) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
         } else if (which == 0) {
             uint32_t bytes = 0;
             if (ge >= 0) bytes += rowb;
@@ -381,18 +387,18 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             if (gf >= 0) bytes += fb;
             mbar_expect_tx(&full[s], bytes);
             if (ge >= 0 && rowb)
-                bulk_g2s(E + (c_lo - xc0), row_at(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
+                bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
             for (int c = c_hi16; c < c_hi; ++c) {
-                if (ge >= 0) E[c - xc0] = row_at(p, in0, ge)[c];
-                if (go >= 0) O[c - xc0] = row_at(p, in0, go)[c];
+                if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
+                if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
             }
             for (int c = f_hi16; c < f_hi; ++c)
-                if (gf >= 0) F[c - X0] = row_at(p, in0, gf)[c];
+                if (gf >= 0) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
         } else if (which == 1) {
             if (go >= 0 && rowb)
-                bulk_g2s(O + (c_lo - xc0), row_at(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+                bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
         } else {
-            if (gf >= 0 && fb) bulk_g2s(F, row_at(p, in0, gf) + X0, fb, &full[s], pol_keep);
+            if (gf >= 0 && fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
         }
     };
     const bool producer = DTB_PAR_PRODUCER ? (warp == 0 && lane < 3) : (t == 0);
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             }
             if (__builtin_expect(unc, 0))
                 fix_uncertain<METHOD>(sPS, sPQ, alpha + V * t, alpha + 2 * p.rx + 1 + V * t,
-                                      row_at(p, in0, y), orow, xo, V, p.cols, ny, p.r, p.N,
+                                      row_at<SEG>(p, in0, y), orow, xo, V, p.cols, ny, p.r, p.N,
                                       p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
         }
         release(k);
@@ -632,7 +638,8 @@ __device__ __forceinline__ void nbar_sync(int id, int count) {
         case 2: nbar_sync_c<2>(count); break;
         case 3: nbar_sync_c<3>(count); break;
         case 4: nbar_sync_c<4>(count); break;
-        default: nbar_sync_c<5>(count); break;
+        case 5: nbar_sync_c<5>(count); break;
+        default: nbar_sync_c<6>(count); break;
     }
 }
 __device__ __forceinline__ void nbar_arrive(int id, int count) {
@@ -640,21 +647,35 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
         case 2: nbar_arrive_c<2>(count); break;
         case 3: nbar_arrive_c<3>(count); break;
         case 4: nbar_arrive_c<4>(count); break;
-        default: nbar_arrive_c<5>(count); break;
+        case 5: nbar_arrive_c<5>(count); break;
+        default: nbar_arrive_c<6>(count); break;
     }
 }
 __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
 }
 
-enum { BAR_COLS = 1, BAR_READY0 = 2, BAR_FREE0 = 4 };
+enum { BAR_COLS = 1, BAR_READY0 = 2, BAR_FREE0 = 4, BAR_WARM = 6 };
+
+#ifndef DTB_WS_SWAP_BUILD
+#define DTB_WS_SWAP_BUILD 0
+#endif
+
+// Warm-up split: the 2r+1 rows that prime a band's column sums are consumed alternately by
+// the column warps (even items) and the otherwise idle output warps (odd items, partial sums
+// for the same columns), which hand their partials over through the not-yet-used prefix area.
+#ifndef DTB_WS_SPLIT_WARM
+#define DTB_WS_SPLIT_WARM 0  // measured no gain on C4 (0.6157 vs 0.6149 ms); kept for A/B
+#endif
 
 #ifndef DTB_WS_MAXREG
 #define DTB_WS_MAXREG 168
 #endif
 
-template <int VO, int RXM4, int METHOD>
+template <int VO, int RXM4, int MX>
 __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
+    constexpr int METHOD = MX & 3;
+    constexpr bool SEG = (MX & 4) != 0;
     constexpr int V = 32;  // columns per column thread (VO: outputs per output thread)
     constexpr int MA = (4 - RXM4) & 3;
     constexpr int MB = (RXM4 + 1) & 3;
@@ -672,10 +693,14 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
     // fixed role slots every sub-partition would host one role only (column warps idle at
     // barriers on two of them while output warps saturate the other two).  Alternate groups
     // of CTAs (role_div = SMs, i.e. one group per residency wave) put the output role first.
+    const int tp = threadIdx.x;
+#if DTB_WS_SWAP_BUILD
     const int bid = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
     const bool swap = p.role_div > 0 && ((bid / p.role_div) & 1);
-    const int tp = threadIdx.x;
     const int t = swap ? (tp < 32 * now ? tp + 32 * ncw : tp - 32 * now) : tp;
+#else
+    const int t = tp;  // role slots fixed (the swap measured slower; build with -DDTB_WS_SWAP_BUILD=1)
+#endif
     const int lane = tp & 31, warp = t >> 5;
     const bool is_col = warp < ncw;
     const uint8_t* in = p.in + (int64_t)blockIdx.z * p.img_stride;
@@ -735,16 +760,16 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
         if (gf >= 0) bytes += fb;
         mbar_expect_tx(&full[s], bytes);
         if (ge >= 0 && rowb)
-            bulk_g2s(E + (c_lo - xc0), row_at(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
+            bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
         if (go >= 0 && rowb)
-            bulk_g2s(O + (c_lo - xc0), row_at(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
-        if (gf >= 0 && fb) bulk_g2s(F, row_at(p, in0, gf) + X0, fb, &full[s], pol_keep);
+            bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+        if (gf >= 0 && fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
         for (int c = c_hi16; c < c_hi; ++c) {
-            if (ge >= 0) E[c - xc0] = row_at(p, in0, ge)[c];
-            if (go >= 0) O[c - xc0] = row_at(p, in0, go)[c];
+            if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
+            if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
         }
         for (int c = f_hi16; c < f_hi; ++c)
-            if (gf >= 0) F[c - X0] = row_at(p, in0, gf)[c];
+            if (gf >= 0) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
     };
 
     if (is_col) {
@@ -756,7 +781,12 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
 #pragma unroll
         for (int j = 0; j < V; ++j) { cS[j] = 0; cQ[j] = 0; }
         uint32_t qS[4] = {0, 0, 0, 0}, qQ[4] = {0, 0, 0, 0};
-        for (int k = 0; k < it.nwarm; ++k) {
+        // warm-up split: column warp c has a helper (output warp c) when c < now; helped warps
+        // take the even items only, unhelped ones every item.  Arrivals per item stay ncw + now.
+        const bool split = DTB_WS_SPLIT_WARM && it.nwarm > 1;
+        const int nh = min(ncw, now);  // helped column warps
+        const bool helped = split && warp < nh;
+        for (int k = 0; k < it.nwarm; k += helped ? 2 : 1) {
             const int s = k % NS;
             mbar_wait(&full[s], (k / NS) & 1);
             const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + V * t);
@@ -773,11 +803,27 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
                 cQ[j] += v * v;
             }
             __syncwarp();
-            // warm-up items are not read by output warps: warp 0 arrives for them as well
-            if (lane == 0) mbar_arrive_cnt(&empty[s], warp == 0 ? 1 + now : 1);
+            // even items: warp 0 also arrives for the output warps; odd items (unhelped warps
+            // only): the output warps arrive for the helped column warps
+            if (lane == 0)
+                mbar_arrive_cnt(&empty[s], (warp == 0 && (!split || (k & 1) == 0)) ? 1 + now : 1);
             if (t == 0)
                 while (issued < min(k + NS, it.n)) issue(issued++);
         }
+#if DTB_WS_SPLIT_WARM
+        if (split) {
+            nbar_sync(BAR_WARM, nthr);  // the helpers' partial sums (odd items) are in smem
+            if (helped) {
+                const uint4* hp = reinterpret_cast<const uint4*>(sm + 2 * V * t);
+#pragma unroll
+                for (int q = 0; q < V / 4; ++q) {
+                    const uint4 a = hp[q], b = hp[V / 4 + q];
+                    cS[4 * q] += a.x; cS[4 * q + 1] += a.y; cS[4 * q + 2] += a.z; cS[4 * q + 3] += a.w;
+                    cQ[4 * q] += b.x; cQ[4 * q + 1] += b.y; cQ[4 * q + 2] += b.z; cQ[4 * q + 3] += b.w;
+                }
+            }
+        }
+#endif
 #pragma unroll
         for (int j = 0; j < V; ++j) { qS[j / (V / 4)] += cS[j]; qQ[j / (V / 4)] += cQ[j]; }
 
@@ -887,6 +933,47 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
         for (int i = 0; i < VO / 4 + 1; ++i) { aw[i] = pchunk_word(la0 + i); bw[i] = pchunk_word(lb0 + i); }
         const bool x_border_warp = __any_sync(0xffffffffu, has_out && !x_interior);
         uint8_t* obase = p.bin + (int64_t)blockIdx.z * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
+#if DTB_WS_SPLIT_WARM
+        if (it.nwarm > 1) {
+            // odd warm-up items: partial column sums for column thread `to`'s columns
+            const int nh = min(ncw, now);
+            const bool helper = to < 32 * nh;
+            uint32_t hS[V], hQ[V];
+#pragma unroll
+            for (int j = 0; j < V; ++j) { hS[j] = 0; hQ[j] = 0; }
+            for (int k = 1; k < it.nwarm; k += 2) {
+                const int s = k % NS;
+                mbar_wait(&full[s], (k / NS) & 1);
+                if (helper) {
+                    const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + V * to);
+                    uint32_t w[V / 4];
+#pragma unroll
+                    for (int q = 0; q < V / 16; ++q) {
+                        const uint4 a = E[q];
+                        w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+                    }
+#pragma unroll
+                    for (int j = 0; j < V; ++j) {
+                        const uint32_t v = byte_at(w, j);
+                        hS[j] += v;
+                        hQ[j] += v * v;
+                    }
+                }
+                __syncwarp();
+                // output warp 0 arrives for the helped column warps, which skip odd items
+                if (lane == 0) mbar_arrive_cnt(&empty[s], (to >> 5) == 0 ? 1 + nh : 1);
+            }
+            if (helper) {
+                uint4* hp = reinterpret_cast<uint4*>(sm + 2 * V * to);
+#pragma unroll
+                for (int q = 0; q < V / 4; ++q) {
+                    hp[q] = make_uint4(hS[4 * q], hS[4 * q + 1], hS[4 * q + 2], hS[4 * q + 3]);
+                    hp[V / 4 + q] = make_uint4(hQ[4 * q], hQ[4 * q + 1], hQ[4 * q + 2], hQ[4 * q + 3]);
+                }
+            }
+            nbar_arrive(BAR_WARM, nthr);
+        }
+#endif
         nbar_arrive(BAR_FREE0, nthr);  // both prefix buffers start free
         nbar_arrive(BAR_FREE0 + 1, nthr);
         for (int k = it.nwarm; k < it.n; ++k) {
@@ -925,7 +1012,7 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
                 }
                 if (__builtin_expect(unc, 0))
                     fix_uncertain<METHOD>(sPS, sPQ, alpha + VO * to, alpha + 2 * p.rx + 1 + VO * to,
-                                          row_at(p, in0, y), orow, xo, VO, p.cols, ny, p.r,
+                                          row_at<SEG>(p, in0, y), orow, xo, VO, p.cols, ny, p.r,
                                           p.N, p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
             }
             __syncwarp();
@@ -1001,15 +1088,20 @@ static int occupancy(int nt, size_t smem) {
 template <int V>
 static cudaError_t dispatch_rx(int m, bool sv, dim3 grid, int nt, size_t smem,
                                const SlideParams& p, cudaStream_t st, int* occ) {
+#define DTB_MX(M, X)                                                                         \
+    if (occ) {                                                                               \
+        *occ = occupancy<V, M, X>(nt, smem);                                                 \
+        return cudaSuccess;                                                                  \
+    }                                                                                        \
+    return run_slide<V, M, X>(grid, nt, smem, p, st);
 #define DTB_CASE(M)                                                                          \
     case M:                                                                                  \
-        if (occ) {                                                                           \
-            *occ = sv ? occupancy<V, M, DTB_METHOD_SAUVOLA>(nt, smem)                         \
-                      : occupancy<V, M, DTB_METHOD_NIBLACK>(nt, smem);                        \
-            return cudaSuccess;                                                              \
+        if constexpr (V == 32) {                                                             \
+            if (p.nseg) {                                                                    \
+                if (sv) { DTB_MX(M, DTB_METHOD_SAUVOLA | 4) } else { DTB_MX(M, DTB_METHOD_NIBLACK | 4) } \
+            }                                                                                \
         }                                                                                    \
-        return sv ? run_slide<V, M, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st)                \
-                  : run_slide<V, M, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st);
+        if (sv) { DTB_MX(M, DTB_METHOD_SAUVOLA) } else { DTB_MX(M, DTB_METHOD_NIBLACK) }
     switch (m) {
         DTB_CASE(0)
         DTB_CASE(1)
@@ -1017,6 +1109,7 @@ static cudaError_t dispatch_rx(int m, bool sv, dim3 grid, int nt, size_t smem,
         DTB_CASE(3)
     }
 #undef DTB_CASE
+#undef DTB_MX
     return cudaErrorInvalidValue;
 }
 
@@ -1062,12 +1155,19 @@ static cudaError_t ws_run(dim3 grid, int nt, size_t smem, const SlideParams& p, 
 template <int VO>
 static cudaError_t ws_dispatch_vo(int m, bool sv, dim3 grid, int nt, size_t smem,
                                   const SlideParams& p, cudaStream_t st, int* occ) {
+#define DTB_WS_M(M)                                                                          \
+    if (p.nseg)                                                                              \
+        return sv ? ws_run<VO, M, DTB_METHOD_SAUVOLA | 4>(grid, nt, smem, p, st, occ)         \
+                  : ws_run<VO, M, DTB_METHOD_NIBLACK | 4>(grid, nt, smem, p, st, occ);        \
+    return sv ? ws_run<VO, M, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ)                 \
+              : ws_run<VO, M, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
     switch (m) {
-        case 0: return sv ? ws_run<VO, 0, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ) : ws_run<VO, 0, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
-        case 1: return sv ? ws_run<VO, 1, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ) : ws_run<VO, 1, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
-        case 2: return sv ? ws_run<VO, 2, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ) : ws_run<VO, 2, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
-        default: return sv ? ws_run<VO, 3, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ) : ws_run<VO, 3, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
+        case 0: { DTB_WS_M(0) }
+        case 1: { DTB_WS_M(1) }
+        case 2: { DTB_WS_M(2) }
+        default: { DTB_WS_M(3) }
     }
+#undef DTB_WS_M
 }
 
 // outputs per output thread: 32 (16 measured slower on B200 and is not exposed)
@@ -1089,7 +1189,7 @@ static int use_ws() {
 
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
     slide_constants(p);
-    const int V = slide_v();
+    const int V = p.nseg ? 32 : slide_v();  // segmented variants exist for V = 32 only
     const int rows_out = p.out_end - p.out_begin;
     const int alpha = (16 - (p.rx & 15)) & 15;
     // strip plan: w warps -> NC = 32 V w columns; pick the w (1..8) with the least total column
