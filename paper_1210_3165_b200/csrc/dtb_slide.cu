@@ -657,6 +657,10 @@ __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
 
 enum { BAR_COLS = 1, BAR_READY0 = 2, BAR_FREE0 = 4, BAR_WARM = 6 };
 
+#ifndef DTB_WS_ISSUE_POS
+#define DTB_WS_ISSUE_POS 2  // C4: 0.6122 (2) vs 0.6153 (0) vs 0.674 (1) ms at 4 stages
+#endif
+
 #ifndef DTB_WS_SWAP_BUILD
 #define DTB_WS_SWAP_BUILD 0
 #endif
@@ -679,7 +683,7 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
     constexpr int V = 32;  // columns per column thread (VO: outputs per output thread)
     constexpr int MA = (4 - RXM4) & 3;
     constexpr int MB = (RXM4 + 1) & 3;
-    constexpr int NS = SLIDE_STAGES;
+    constexpr int NS = WS_STAGES;
     extern __shared__ __align__(128) uint32_t sm[];
     const int NCp = slide_padded_words(p.NC);
     uint32_t* sWS = sm + 4 * NCp;   // [2][8] per-column-warp totals, double buffered
@@ -877,8 +881,14 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
             for (int w = 0; w < warp; ++w) { bS += sWS[8 * b + w]; bQ += sWQ[8 * b + w]; }
             // wait until the output warps have consumed row k-2 from this prefix buffer
             nbar_sync(BAR_FREE0 + b, nthr);
-            if (t == 0)
+            // Row staging for a later row.  Issuing item j needs item j-NS released by every
+            // warp; FREE(k-2) guarantees that for j <= k+NS-2, so ISSUE_POS 1 never stalls the
+            // producer here, while ISSUE_POS 0 (lookahead NS-1) can hold column warp 0 -- and
+            // with it READY(k) -- until the output warps finish row k-1.
+            if (DTB_WS_ISSUE_POS == 0 && t == 0)
                 while (issued < min(k + NS - 1, it.n)) issue(issued++);
+            if (DTB_WS_ISSUE_POS == 1 && t == 0)
+                while (issued < min(k + NS - 2, it.n)) issue(issued++);
             uint32_t* sPS = sm + (2 * b) * NCp;
             uint32_t* sPQ = sm + (2 * b + 1) * NCp;
             uint32_t cbS[4], cbQ[4];
@@ -911,6 +921,8 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
                 sPQ[pw] = cbQ[3];
             }
             nbar_arrive(BAR_READY0 + b, nthr);
+            if (DTB_WS_ISSUE_POS == 2 && t == 0)  // after publishing row k: off READY's path
+                while (issued < min(k + NS - 1, it.n)) issue(issued++);
         }
         // consume the output warps' last FREE arrivals so no named barrier is left pending
         const int rows = it.n - it.nwarm;

@@ -34,9 +34,14 @@ struct SlideParams {
     int role_div;      // ws: swap the two roles' warp slots in every other group of role_div CTAs (0 = never)
 };
 
+#ifndef WS_STAGES
+#define WS_STAGES 6  // ws_kernel ring depth (C4: 0.6094 ms at 6 vs 0.6122 at 4, issue after READY)
+#endif
+static_assert(WS_STAGES >= 3, "the ring protocol needs at least 3 stages");
 #ifndef SLIDE_STAGES
 #define SLIDE_STAGES 4
 #endif
+static_assert(SLIDE_STAGES >= 3, "the ring protocol needs at least 3 stages");
 
 // Words of one padded prefix array (logical 16-byte chunk L stored at chunk L + L/8).
 __host__ __device__ inline int slide_padded_words(int NC) {
@@ -52,9 +57,9 @@ __host__ __device__ inline size_t slide_smem_bytes(int NC) {
 }
 
 // Warp-specialized kernel: two prefix buffers instead of one.
-__host__ __device__ inline size_t ws_smem_bytes(int NC) {
+__host__ __device__ inline size_t ws_smem_bytes(int NC) {  // uses WS_STAGES
     return sizeof(uint32_t) * (4 * (size_t)slide_padded_words(NC) + 32) +
-           2 * SLIDE_STAGES * sizeof(uint64_t) + (size_t)SLIDE_STAGES * 3 * NC;
+           2 * WS_STAGES * sizeof(uint64_t) + (size_t)WS_STAGES * 3 * NC;
 }
 
 // Fills N / cA / cC / tol from (r, method, k, rr) -- see the error analysis in dtb_slide.cu.
