@@ -212,7 +212,7 @@ def run_ours(a):
         peers = [D.PeerHalos(bands[j], w["rows"], r) for j in range(nrot)] if use_p2p else None
         if use_p2p:
             peers[0].barrier()
-        w["halo"] = ("none (1 GPU)" if world == 1 else
+        w["halo_transport"] = ("none (1 GPU)" if world == 1 else
                      "read in place from the neighbours' HBM over NVLink (CUDA IPC), fused into "
                      "the kernel's row staging" if use_p2p else "NCCL send/recv copy per step")
         launches_per_step = 1
@@ -339,7 +339,7 @@ def run_ours(a):
             "config": {"workload": w["desc"], "image": w["shape"], "window": w["win"],
                        "method": w["method"], "k": w["k"], "r": w["r"],
                        "parallelism": f"{'rowband' if w['kind'] == 'rowband' else 'image'}{world}",
-                       **({"halo": w["halo"]} if "halo" in w else {}),
+                       **({"halo": w["halo_transport"]} if "halo_transport" in w else {}),
                        "l2": (f"{nrot} rotating input/output buffer sets, "
                               f"{nrot * per_step_bytes / 2**20:.0f} MiB per rank >= 2x L2 "
                               f"({l2 / 2**20:.0f} MiB)")},

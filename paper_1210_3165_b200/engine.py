@@ -87,6 +87,68 @@ def binarize(gray, win: int, method: str, k: float, r: float, want_tmap: bool = 
     return out, tmap
 
 
+_side_streams = {}
+
+
+def _streams_for(dev):
+    """(copy-in, copy-out) side streams for a device, created once."""
+    torch = torch_mod()
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _side_streams:
+        with torch.cuda.device(key):
+            _side_streams[key] = (torch.cuda.Stream(), torch.cuda.Stream())
+    return _side_streams[key]
+
+
+def host_streamed(host, band_fn, rad: int, out=None, chunk_rows: int | None = None):
+    """Host page -> host binary with H2D, compute and D2H overlapped by row chunks.
+
+    ``host`` is a (rows, cols) uint8 CPU tensor (pinned for real overlap).  Row chunk i is
+    copied in on one side stream, computed on the current stream as soon as the input rows
+    its windows reach (chunk end + rad) have landed, and copied out on another side stream
+    while later chunks compute -- PCIe's two directions run concurrently instead of
+    back to back.  ``band_fn(dev_in, y0, y1, dev_out_rows)`` computes output rows [y0, y1)
+    from the full-page device buffer.  Returns the host result (synchronised).
+    """
+    torch = torch_mod()
+    h, w = host.shape
+    if out is None:
+        out = torch.empty((h, w), dtype=torch.uint8, pin_memory=host.is_pinned())
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cur = torch.cuda.current_stream()
+    s_in, s_out = _streams_for(dev)
+    dev_in = torch.empty((h, w), dtype=torch.uint8, device=dev)
+    dev_out = torch.empty((h, w), dtype=torch.uint8, device=dev)
+    if chunk_rows is None:
+        import os
+        n = int(os.environ.get("DTB_STREAM_CHUNKS", "16"))
+        chunk_rows = max(256, -(-h // n))
+    bounds = [(a, min(a + chunk_rows, h)) for a in range(0, h, chunk_rows)]
+    s_in.wait_stream(cur)
+    s_out.wait_stream(cur)
+    ev_in = []
+    with torch.cuda.stream(s_in):
+        for a, b in bounds:
+            dev_in[a:b].copy_(host[a:b], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(s_in)
+            ev_in.append(e)
+    for a, b in bounds:
+        need = min(b + rad, h)
+        cur.wait_event(ev_in[(need - 1) // chunk_rows])
+        band_fn(dev_in, a, b, dev_out[a:b])
+        e = torch.cuda.Event()
+        e.record(cur)
+        s_out.wait_event(e)
+        with torch.cuda.stream(s_out):
+            out[a:b].copy_(dev_out[a:b], non_blocking=True)
+    dev_in.record_stream(s_in)
+    dev_out.record_stream(s_out)
+    cur.wait_stream(s_out)
+    cur.synchronize()
+    return out
+
+
 def binarize_band(buf, row0_global: int, rows_global: int, out_begin: int, out_end: int,
                   win: int, method: str, k: float, r: float, out=None, stream=None):
     """Binarize global rows [out_begin, out_end) from a buffer holding rows [row0, row0+len)."""
