@@ -657,6 +657,10 @@ __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
 
 enum { BAR_COLS = 1, BAR_READY0 = 2, BAR_FREE0 = 4, BAR_WARM = 6 };
 
+#ifndef DTB_WS_UNIFORM_OFFS
+#define DTB_WS_UNIFORM_OFFS 0  // C4: 0.6165 (1) vs 0.6086 (0) ms -- the compiler keeps them per-thread anyway
+#endif
+
 #ifndef DTB_WS_ISSUE_POS
 #define DTB_WS_ISSUE_POS 2  // C4: 0.6122 (2) vs 0.6153 (0) vs 0.674 (1) ms at 4 stages
 #endif
@@ -938,11 +942,29 @@ __global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
                               ((reinterpret_cast<uintptr_t>(p.bin) | (uintptr_t)p.bin_pitch |
                                 (uintptr_t)p.out_stride) & 15) == 0;
         const bool x_interior = (p.rx == p.r) && (xo - p.r >= 0) && (xo + VO - 1 + p.r <= p.cols - 1);
+#if DTB_WS_UNIFORM_OFFS
+        // Run chunk addresses = per-thread base + launch-uniform offsets: thread `to`'s A run
+        // starts at chunk 8*to + dA (dA = (alpha - MA)/4 in 0..3, the same for every thread),
+        // and pchunk_word(8*to + d) = 36*to + 4*(d + d/8) for d >= 0, so the compiler can keep
+        // the 2 x 9 offsets in uniform registers instead of per-thread ones.
+        static_assert(VO == 32, "uniform run offsets assume 8 chunks per output thread");
+        const int dA = (alpha - MA) >> 2, dB = (alpha + 2 * p.rx + 1 - MB) >> 2;
+        const int tb = 36 * to;
+        int aw[VO / 4 + 1], bw[VO / 4 + 1];
+#pragma unroll
+        for (int i = 0; i < VO / 4 + 1; ++i) {
+            aw[i] = tb + 4 * (dA + i + ((dA + i) >> 3));
+            bw[i] = tb + 4 * (dB + i + ((dB + i) >> 3));
+            DTB_CHECK(aw[i] == pchunk_word(((alpha + VO * to - MA) >> 2) + i));
+            DTB_CHECK(bw[i] == pchunk_word(((alpha + 2 * p.rx + 1 + VO * to - MB) >> 2) + i));
+        }
+#else
         const int la0 = (alpha + VO * to - MA) >> 2;
         const int lb0 = (alpha + 2 * p.rx + 1 + VO * to - MB) >> 2;
         int aw[VO / 4 + 1], bw[VO / 4 + 1];
 #pragma unroll
         for (int i = 0; i < VO / 4 + 1; ++i) { aw[i] = pchunk_word(la0 + i); bw[i] = pchunk_word(lb0 + i); }
+#endif
         const bool x_border_warp = __any_sync(0xffffffffu, has_out && !x_interior);
         uint8_t* obase = p.bin + (int64_t)blockIdx.z * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
 #if DTB_WS_SPLIT_WARM
