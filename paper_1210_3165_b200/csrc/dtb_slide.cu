@@ -1221,6 +1221,19 @@ static int use_ws() {
     return v;
 }
 
+// Debug / tuning knobs read once: DTB_PRINT_PLAN=1 prints each launch's strip/band plan;
+// DTB_BAND_SCALE scales the band count (1 = one full wave of resident CTAs).
+static bool print_plan() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("DTB_PRINT_PLAN"); v = (e && e[0] == '1') ? 1 : 0; }
+    return v == 1;
+}
+static double band_scale() {
+    static double v = -1.0;
+    if (v < 0) { const char* e = getenv("DTB_BAND_SCALE"); v = e ? atof(e) : 1.0; if (!(v > 0)) v = 1.0; }
+    return v;
+}
+
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
     slide_constants(p);
     const int V = p.nseg ? 32 : slide_v();  // segmented variants exist for V = 32 only
@@ -1265,10 +1278,13 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         int occ = 1;
         ws_dispatch(m, sv, dim3(), nt, smem, p, st, &occ);
         const int slots = num_sms * occ;
-        int nbands = std::max(1, slots / std::max(1, best_strips * n_images));
+        int nbands = std::max(1, (int)(band_scale() * slots / std::max(1, best_strips * n_images)));
         nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
         p.TH = (rows_out + nbands - 1) / nbands;
         dim3 grid(best_strips, (rows_out + p.TH - 1) / p.TH, n_images);
+        if (print_plan())
+            fprintf(stderr, "[dtb plan] ws_kernel cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d\n",
+                    p.cols, rows_out, p.r, best_w, best_strips, best_tw, occ, (int)grid.y, p.TH);
         return ws_dispatch(m, sv, grid, nt, smem, p, st, nullptr);
     }
     const int nt = 32 * best_w;
@@ -1284,10 +1300,13 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // bands: one full wave of resident CTAs (bands as tall as possible: the warm-up of each
     // band costs 2r+1 rows of vertical work)
     const int slots = num_sms * occ;
-    int nbands = std::max(1, slots / std::max(1, nstrips * n_images));
+    int nbands = std::max(1, (int)(band_scale() * slots / std::max(1, nstrips * n_images)));
     nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
     p.TH = (rows_out + nbands - 1) / nbands;
     dim3 grid(nstrips, (rows_out + p.TH - 1) / p.TH, n_images);
+    if (print_plan())
+        fprintf(stderr, "[dtb plan] slide_kernel V=%d cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d\n",
+                V, p.cols, rows_out, p.r, best_w, nstrips, best_tw, occ, (int)grid.y, p.TH);
     return V == 16 ? dispatch_rx<16>(m, sv, grid, nt, smem, p, st, nullptr)
                    : dispatch_rx<32>(m, sv, grid, nt, smem, p, st, nullptr);
 }
