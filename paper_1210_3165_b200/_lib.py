@@ -48,6 +48,8 @@ SIGNATURES = {
     "dtb_ipc_export": [_c_p, _c_p, _c_p],
     "dtb_ipc_import": [_c_p, _c_p],
     "dtb_ipc_close": [_c_p],
+    "dtb_gs_band": [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
+                    _c_p, _c_i64, _c_i32, _c_f64, _c_f64, _c_p],
     "dtb_confusion": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
     "dtb_sweep_counts": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p,
                          _c_i32, _c_i32, _c_f64, _c_p, _c_p],

@@ -58,6 +58,9 @@ struct GsParams {
     double* tmap;
     int method;
     double k, rr;
+    int row0;       // global row held by buffer row 0 (row bands; 0 for a whole image)
+    int in_rows;    // rows in the buffer
+    int y0, y1;     // output rows [y0, y1) (global); outputs are stored from row y0
     int nmask;      // |mask| = the count of every unclipped window
     int fast;       // binary only (no tmap / stats): certified fp32 decision
     FastConsts fc;  // for the interior count |mask|
@@ -193,7 +196,7 @@ __device__ __forceinline__ void gs_fast_interior(const GsParams& p, const uint8_
                                                  const uint32_t (&vq)[GS_SEG], int i0, int j,
                                                  int tx0, int ty0) {
     const int r = p.r, pw = p.pw;
-    uint8_t* out = p.bin + (int64_t)(ty0 + i0) * p.bin_pitch + tx0 + j;
+    uint8_t* out = p.bin + (int64_t)(ty0 + i0 - p.y0) * p.bin_pitch + tx0 + j;
 #pragma unroll
     for (int u = 0; u < GS_SEG; ++u) {
         const int i = i0 + u;
@@ -219,19 +222,21 @@ __global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
     uint2* edge_m = edge_p + GS_TY;
     uint8_t* tile = reinterpret_cast<uint8_t*>(edge_m + GS_TY);
 
-    const int ty0 = blockIdx.y * GS_TY, tx0 = blockIdx.x * GS_TX;
+    const int ty0 = p.y0 + blockIdx.y * GS_TY, tx0 = blockIdx.x * GS_TX;
+    const uint8_t* in0 = p.in - (int64_t)p.row0 * p.pitch;  // global row g at in0 + g * pitch
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // Interior tile: every window of every output is unclipped (count = |mask|), and the
     // staged rows are followed by at least one more image row (the word loads below may run
     // up to 7 bytes past a staged row's end).
-    const bool interior = ty0 >= r && ty0 + GS_TY + r < p.rows && tx0 >= r &&
-                          tx0 + GS_TX + r <= p.cols;
+    const bool interior = ty0 >= r && ty0 + GS_TY + r <= p.rows &&
+                          ty0 + GS_TY + r < p.row0 + p.in_rows && ty0 + GS_TY <= p.y1 &&
+                          tx0 >= r && tx0 + GS_TX + r <= p.cols;
     // Stage the padded tile (zero outside the image).
     if (interior) {
         // aligned 4-byte loads, realigned with a funnel shift, 4-byte shared stores
         const int nw = (PC + 3) >> 2;
         for (int pr = warp; pr < PR; pr += GS_NT / 32) {
-            const uintptr_t ad = reinterpret_cast<uintptr_t>(p.in + (int64_t)(ty0 - r + pr) * p.pitch +
+            const uintptr_t ad = reinterpret_cast<uintptr_t>(in0 + (int64_t)(ty0 - r + pr) * p.pitch +
                                                              (tx0 - r));
             const uint32_t* w = reinterpret_cast<const uint32_t*>(ad & ~(uintptr_t)3);
             const uint32_t sh = (uint32_t)(ad & 3) * 8u;
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
         for (int pr = warp; pr < PR; pr += GS_NT / 32) {
             const int gy = ty0 - r + pr;
             const bool rowok = gy >= 0 && gy < p.rows;
-            const uint8_t* src = p.in + (int64_t)gy * p.pitch;
+            const uint8_t* src = in0 + (int64_t)gy * p.pitch;
             for (int pc = lane; pc < PC; pc += 32) {
                 const int gx = tx0 - r + pc;
                 tile[pr * pw + pc] = (rowok && gx >= 0 && gx < p.cols) ? __ldg(src + gx) : 0;
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
 #pragma unroll 1
     for (int u = 0; u < GS_SEG; ++u) {
         const int i = i0 + u, y = ty0 + i;
-        if (y >= p.rows) break;
+        if (y >= p.y1) break;
         const uint2 a = acc[i * GS_ACC + j];
         uint32_t S = a.x, Q = a.y;
         const uint32_t f = tile[(i + r) * pw + j + r];
@@ -362,18 +367,18 @@ __global__ void __launch_bounds__(GS_NT) gs_kernel(GsParams p) {
                                  : fast_diff<DTB_METHOD_NIBLACK, true>(S, Q, f, un, p.fc.cA, p.fc.cC, p.fc.a, p.fc.c);
             const uint32_t white = fabsf(d) >= p.fc.tol ? (d < 0.f ? 0u : 255u)
                                                         : exact_white(S, Q, (double)n, f, p.method, p.k, p.rr);
-            p.bin[(int64_t)y * p.bin_pitch + x] = (uint8_t)white;
+            p.bin[(int64_t)(y - p.y0) * p.bin_pitch + x] = (uint8_t)white;
             continue;
         }
         double mean, sd;
         finish_exact((double)S, (double)Q, (double)n, mean, sd);
-        const int64_t idx = (int64_t)y * cols + x;
+        const int64_t idx = (int64_t)(y - p.y0) * cols + x;
         if (p.mean) p.mean[idx] = mean;
         if (p.sd) p.sd[idx] = sd;
         if (p.cnt) p.cnt[idx] = n;
         if (p.bin) {
             const double t = threshold_exact(mean, sd, p.method, p.k, p.rr);
-            p.bin[(int64_t)y * p.bin_pitch + x] = ((double)f < t) ? 0 : 255;
+            p.bin[(int64_t)(y - p.y0) * p.bin_pitch + x] = ((double)f < t) ? 0 : 255;
             if (p.tmap) p.tmap[idx] = t;
         }
     }
@@ -388,40 +393,28 @@ size_t gs_smem_bytes(int r) {
     return sizeof(uint2) * (GS_TY * GS_ACC + 2 * GS_TY) + (size_t)(GS_TY + 2 * r) * gs_pitch(r);
 }
 
-}  // namespace dtb
-
-using namespace dtb;
-
-extern "C" {
-
-int dtb_gs_stats(const uint8_t* gray, int64_t pitch, int32_t rows, int32_t cols, int32_t structure,
-                 int32_t win, double* mean, double* std_, int32_t* count, uint8_t* binary,
-                 int64_t binary_pitch, double* tmap, int32_t method, double k, double r,
-                 void* stream) {
-    if (!gray) return fail(DTB_E_INVALID, "null pointer");
-    if (rows <= 0 || cols <= 0) return fail(DTB_E_INVALID, "image is empty");
-    if (win < 3 || win % 2 == 0) return fail(DTB_E_INVALID, "window: must be an odd integer >= 3, got %d", win);
+// Shared launcher: p has the image/band fields, outputs and method set.
+static int gs_run(GsParams p, int structure, int win, void* stream) {
     if (structure < DTB_GS1 || structure > DTB_GS6)
         return fail(DTB_E_INVALID, "structure: expected DTB_GS1..DTB_GS6, got %d", structure);
-    if (!binary && !mean && !std_ && !count) return fail(DTB_E_INVALID, "no output requested");
-    if (binary && method != DTB_METHOD_SAUVOLA && method != DTB_METHOD_NIBLACK)
-        return fail(DTB_E_INVALID, "method: unknown code %d", method);
-    if (pitch < cols || (binary && binary_pitch < cols))
-        return fail(DTB_E_INVALID, "pitch smaller than the row width");
+    if (win < 3 || win % 2 == 0) return fail(DTB_E_INVALID, "window: must be an odd integer >= 3, got %d", win);
+    if (p.bin && p.method != DTB_METHOD_SAUVOLA && p.method != DTB_METHOD_NIBLACK)
+        return fail(DTB_E_INVALID, "method: unknown code %d", p.method);
     const int rad = win / 2;
     const size_t smem = gs_smem_bytes(rad);
     if (smem > DTB_GS_MAX_SMEM)
         return fail(DTB_E_UNSUPPORTED, "window %d too large for the tiled GS kernel", win);
-    GsParams p{gray, pitch, rows, cols, rad, gs_pitch(rad), mean, std_, count, binary,
-               binary_pitch, tmap, method, k, r, 0, 0, FastConsts{}};
+    p.r = rad;
+    p.pw = gs_pitch(rad);
     static const int mul[7] = {0, 2, 2, 4, 3, 4, 6};  // |mask| = mul*W - sub (masks.py:5-12)
     static const int sub[7] = {0, 1, 1, 3, 2, 3, 9};
     p.nmask = mul[structure] * win - sub[structure];
-    if (binary && !tmap && !mean && !std_ && !count) {
+    if (p.bin && !p.tmap && !p.mean && !p.sd && !p.cnt) {
         p.fast = 1;
-        p.fc = fast_constants(method, k, r, (double)p.nmask);
+        p.fc = fast_constants(p.method, p.k, p.rr, (double)p.nmask);
     }
-    const dim3 grid((cols + GS_TX - 1) / GS_TX, (rows + GS_TY - 1) / GS_TY);
+    if (p.y1 <= p.y0) return DTB_OK;
+    const dim3 grid((p.cols + GS_TX - 1) / GS_TX, (p.y1 - p.y0 + GS_TY - 1) / GS_TY);
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
 #define DTB_GS_LAUNCH(G)                                                                      \
@@ -442,6 +435,52 @@ int dtb_gs_stats(const uint8_t* gray, int64_t pitch, int32_t rows, int32_t cols,
 #undef DTB_GS_LAUNCH
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? DTB_OK : cuda_fail(e, "gs_kernel launch");
+}
+
+}  // namespace dtb
+
+using namespace dtb;
+
+extern "C" {
+
+int dtb_gs_stats(const uint8_t* gray, int64_t pitch, int32_t rows, int32_t cols, int32_t structure,
+                 int32_t win, double* mean, double* std_, int32_t* count, uint8_t* binary,
+                 int64_t binary_pitch, double* tmap, int32_t method, double k, double r,
+                 void* stream) {
+    if (!gray) return fail(DTB_E_INVALID, "null pointer");
+    if (rows <= 0 || cols <= 0) return fail(DTB_E_INVALID, "image is empty");
+    if (!binary && !mean && !std_ && !count) return fail(DTB_E_INVALID, "no output requested");
+    if (pitch < cols || (binary && binary_pitch < cols))
+        return fail(DTB_E_INVALID, "pitch smaller than the row width");
+    GsParams p{};
+    p.in = gray; p.pitch = pitch; p.rows = rows; p.cols = cols;
+    p.row0 = 0; p.in_rows = rows; p.y0 = 0; p.y1 = rows;
+    p.mean = mean; p.sd = std_; p.cnt = count; p.bin = binary; p.bin_pitch = binary_pitch;
+    p.tmap = tmap; p.method = method; p.k = k; p.rr = r;
+    return gs_run(p, structure, win, stream);
+}
+
+int dtb_gs_band(const uint8_t* gray, int64_t pitch, int32_t in_rows, int32_t cols,
+                int32_t row0_global, int32_t rows_global, int32_t out_row_begin,
+                int32_t out_row_end, int32_t structure, int32_t win, uint8_t* binary,
+                int64_t binary_pitch, int32_t method, double k, double r, void* stream) {
+    if (!gray || !binary) return fail(DTB_E_INVALID, "null image pointer");
+    if (cols <= 0 || rows_global <= 0) return fail(DTB_E_INVALID, "image is empty");
+    if (pitch < cols || binary_pitch < cols) return fail(DTB_E_INVALID, "pitch smaller than the row width");
+    if (out_row_begin < 0 || out_row_end > rows_global || out_row_begin > out_row_end)
+        return fail(DTB_E_INVALID, "rows: output rows [%d,%d) outside image of %d rows",
+                    out_row_begin, out_row_end, rows_global);
+    const int rad = win / 2;
+    const int need0 = std::max(out_row_begin - rad, 0);
+    const int need1 = std::min(out_row_end + rad, (int)rows_global);
+    if (out_row_end > out_row_begin && (need0 < row0_global || need1 > row0_global + in_rows))
+        return fail(DTB_E_INVALID, "rows: band needs global rows [%d,%d) but buffer holds [%d,%d)",
+                    need0, need1, row0_global, row0_global + in_rows);
+    GsParams p{};
+    p.in = gray; p.pitch = pitch; p.rows = rows_global; p.cols = cols;
+    p.row0 = row0_global; p.in_rows = in_rows; p.y0 = out_row_begin; p.y1 = out_row_end;
+    p.bin = binary; p.bin_pitch = binary_pitch; p.method = method; p.k = k; p.rr = r;
+    return gs_run(p, structure, win, stream);
 }
 
 }  // extern "C"

@@ -98,17 +98,19 @@ def exchange_halos(band: torch.Tensor, rows: int, r: int, group=None,
 def binarize_rowbands(band: torch.Tensor, rows: int, win: int, method: str, k: float,
                       r: float, group=None, compute: Callable | None = None,
                       halo_buf: torch.Tensor | None = None, out: torch.Tensor | None = None,
-                      transport: str = "nccl"):
+                      transport: str = "nccl", structure: str | None = None):
     """This rank's binarized rows [y0, y1) of a page split in row bands across the group.
 
     transport "nccl" copies the halos first (exchange_halos); "p2p" maps the neighbours'
     bands through CUDA IPC for this one call and reads the halos in place (for repeated
-    steps keep a ``PeerHalos`` instead, which maps once).
+    steps keep a ``PeerHalos`` instead, which maps once).  ``structure`` ("gs1".."gs6")
+    selects the GS-mask engine (reference default) instead of the full window; it uses the
+    NCCL transport.
     """
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     y0, y1 = band_bounds(rows, world, rank)
-    if transport == "p2p" and compute is None:
+    if transport == "p2p" and compute is None and structure is None:
         ph = PeerHalos(band, rows, win // 2, group)
         try:
             res = ph.binarize(win, method, k, r, out=out)
@@ -119,6 +121,8 @@ def binarize_rowbands(band: torch.Tensor, rows: int, win: int, method: str, k: f
     buf, a = exchange_halos(band, rows, win // 2, group, out=halo_buf)
     if compute is None:
         from . import engine
+        if structure is not None:  # GS-mask ("sampled") engine
+            return engine.gs_band(buf, a, rows, y0, y1, structure, win, method, k, r, out=out)
         return engine.binarize_band(buf, a, rows, y0, y1, win, method, k, r, out=out)
     return compute(buf, a, rows, y0, y1, win, method, k, r)
 

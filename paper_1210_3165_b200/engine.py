@@ -311,6 +311,29 @@ def gs(gray, structure: str, win: int, method: str | None = None, k: float = 0.0
     return res
 
 
+def gs_band(buf, row0_global: int, rows_global: int, out_begin: int, out_end: int,
+            structure: str, win: int, method: str, k: float, r: float, out=None, stream=None):
+    """GS-mask binarization of global rows [out_begin, out_end) from a row-band buffer
+    (dtb_gs_band); windows clip at the page's global borders."""
+    torch = torch_mod()
+    g = to_device(buf)
+    in_rows, w = g.shape
+    if out is None:
+        out = torch.empty((out_end - out_begin, w), dtype=torch.uint8, device=g.device)
+    rc = _lib.lib().dtb_gs_band(g.data_ptr(), g.stride(0), in_rows, w, int(row0_global),
+                                int(rows_global), int(out_begin), int(out_end),
+                                GS_CODES[structure], int(win), out.data_ptr(), out.stride(0),
+                                METHOD_CODES[method], float(k), float(r), _stream(stream))
+    if rc == _lib.DTB_E_UNSUPPORTED and (row0_global, in_rows) == (0, rows_global):
+        # window too wide for the tiled kernel: the offset-gather kernel on the whole page
+        from .masks import make_mask
+        full, _ = sampled(g, make_mask(structure, win).offsets, method, k, r, want_tmap=False)
+        out.copy_(full[out_begin:out_end])
+        return out
+    _lib.check(rc, "dtb_gs_band")
+    return out
+
+
 def to_gray(rgb, stream=None):
     torch = torch_mod()
     t = to_device(rgb, ndim=3, what="rgb")

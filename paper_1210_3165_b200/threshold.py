@@ -140,12 +140,19 @@ def binarize(img, params: BinarizationParams = BinarizationParams(), *, return_t
     src = img
     img, host = _validated(img)
     params.validate()
-    if (engine.is_host_tensor(src) and params.method != "otsu" and params.full_window
-            and not return_tmap and src.is_contiguous()):
+    if (engine.is_host_tensor(src) and params.method != "otsu" and not return_tmap
+            and src.is_contiguous()):
         # pinned host page: H2D / compute / D2H overlapped by row chunks (engine.host_streamed)
-        def band(dev_in, y0, y1, dev_out):
-            engine.binarize_band(dev_in, 0, dev_in.shape[0], y0, y1, params.window,
-                                 params.method, params.k, params.r, out=dev_out)
+        if params.full_window:
+            def band(dev_in, y0, y1, dev_out):
+                engine.binarize_band(dev_in, 0, dev_in.shape[0], y0, y1, params.window,
+                                     params.method, params.k, params.r, out=dev_out)
+        else:
+            structure = make_mask(params.mask, params.window).structure
+
+            def band(dev_in, y0, y1, dev_out):
+                engine.gs_band(dev_in, 0, dev_in.shape[0], y0, y1, structure, params.window,
+                               params.method, params.k, params.r, out=dev_out)
         return engine.host_streamed(src, band, params.window // 2, out=out), None
     dev = engine.to_device(img)
     if params.method == "otsu":

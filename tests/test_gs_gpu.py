@@ -84,3 +84,31 @@ def test_gs_fast_path_near_ties(rng, structure):
             tm = numpy_ref.threshold_map(om, os_, method, k)
             want = np.where(img.astype(np.float64) < tm, 0, 255).astype(np.uint8)
             assert np.array_equal(b.cpu().numpy(), want), (method, k, win)
+
+
+@pytest.mark.parametrize("structure", STRUCTS)
+@pytest.mark.parametrize("win", [3, 21, 63, 127])
+def test_gs_bands_stitch_to_whole_page(rng, structure, win):
+    """dtb_gs_band over row bands whose buffers hold only the band + r-row halos."""
+    import torch
+    h, w = 517, 700
+    img = torch.from_numpy(_doc(rng, h, w)).cuda()
+    want, _ = engine.gs(img, structure, win, "sauvola", 0.34, 128.0, want_tmap=False)
+    r = win // 2
+    cuts = [0, 1, 40, 41, 200, 333, 516, 517]
+    for y0, y1 in zip(cuts[:-1], cuts[1:]):
+        a, z = max(y0 - r, 0), min(y1 + r, h)
+        buf = img[a:z].clone()
+        got = engine.gs_band(buf, a, h, y0, y1, structure, win, "sauvola", 0.34, 128.0)
+        assert torch.equal(got, want[y0:y1]), (y0, y1)
+
+
+def test_default_params_host_tensor_streamed(rng):
+    """binarize(pinned host tensor) with the reference defaults (gs3 W=21) streams row
+    chunks through dtb_gs_band and equals the device result."""
+    import torch
+    img = _doc(rng, 1500, 1234)
+    want, _ = dt.binarize(torch.from_numpy(img).cuda(), return_tmap=False)
+    host = torch.from_numpy(img).pin_memory()
+    got, t = dt.binarize(host, return_tmap=False)
+    assert t is None and torch.equal(got, want.cpu())
