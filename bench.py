@@ -185,10 +185,20 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only plumbing: DTB_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 and
+    # DTB_BENCH_BACKEND=gloo avoids NCCL's one-rank-per-GPU rule, so the N>1 code path (p2p
+    # halo mapping, max-over-ranks timing) can be exercised on a one-GPU box.  Numbers from
+    # such a run are not measurements.
+    backend = os.environ.get("DTB_BENCH_BACKEND", "nccl")
+    if os.environ.get("DTB_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     w = workload(a.config, world, rank, a.scaling, a.window)
     props = torch.cuda.get_device_properties(dev)
     l2 = int(getattr(props, "L2_cache_size", 126 * 2**20))
@@ -272,7 +282,10 @@ def run_ours(a):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     sampler = ClockSampler(None) if rank == 0 else None
     for i in range(a.warmup):
@@ -296,7 +309,7 @@ def run_ours(a):
     ms = t0.elapsed_time(t1) / a.steps
     kms = statistics.fmean(s.elapsed_time(e) for s, e in kev)
     if world > 1:
-        t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, kms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kms = float(t[0]), float(t[1])
     total_px = w["px_rank"] * world if a.scaling == "weak" or w["kind"] != "rowband" else (
@@ -417,7 +430,8 @@ def run_e2e(a, w, world, rank, local, dev, barrier):
     ms = t0.elapsed_time(t1) / steps
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        on_dev = os.environ.get("DTB_BENCH_BACKEND", "nccl") == "nccl"
+        t = torch.tensor([ms], dtype=torch.float64, device=dev if on_dev else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     px = w["px_rank"] * world
