@@ -657,6 +657,10 @@ __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
 
 enum { BAR_COLS = 1, BAR_READY0 = 2, BAR_FREE0 = 4, BAR_WARM = 6 };
 
+#ifndef DTB_WS_V16_DEFAULT
+#define DTB_WS_V16_DEFAULT 0  // C4: 0.759 ms with V = VO = 16 (24 warps/SM) vs 0.609 with 32 (12)
+#endif
+
 #ifndef DTB_WS_UNIFORM_OFFS
 #define DTB_WS_UNIFORM_OFFS 0  // C4: 0.6165 (1) vs 0.6086 (0) ms -- the compiler keeps them per-thread anyway
 #endif
@@ -679,12 +683,17 @@ enum { BAR_COLS = 1, BAR_READY0 = 2, BAR_FREE0 = 4, BAR_WARM = 6 };
 #ifndef DTB_WS_MAXREG
 #define DTB_WS_MAXREG 168
 #endif
+#ifndef DTB_WS_MAXREG16
+#define DTB_WS_MAXREG16 80
+#endif
 
-template <int VO, int RXM4, int MX>
-__global__ void __maxnreg__(DTB_WS_MAXREG) ws_kernel(SlideParams p) {
+// V: columns per column thread; VO: outputs per output thread.  V = VO = 32 (168 registers,
+// 3 CTAs x 4 warps per SM) or V = VO = 16 (half the per-thread state, DTB_WS_MAXREG16
+// registers, twice the warps per CTA).
+template <int V, int VO, int RXM4, int MX>
+__global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel(SlideParams p) {
     constexpr int METHOD = MX & 3;
     constexpr bool SEG = (MX & 4) != 0;
-    constexpr int V = 32;  // columns per column thread (VO: outputs per output thread)
     constexpr int MA = (4 - RXM4) & 3;
     constexpr int MB = (RXM4 + 1) & 3;
     constexpr int NS = WS_STAGES;
@@ -1158,11 +1167,11 @@ static int slide_v() {
 
 
 // ---- warp-specialized launcher
-template <int VO, int RXM4, int METHOD>
+template <int V, int VO, int RXM4, int MX>
 static cudaError_t ws_run(dim3 grid, int nt, size_t smem, const SlideParams& p, cudaStream_t st,
                           int* occ) {
     static size_t granted = 48 * 1024;
-    auto kern = ws_kernel<VO, RXM4, METHOD>;
+    auto kern = ws_kernel<V, VO, RXM4, MX>;
     if (smem > granted) {
         const cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1186,15 +1195,15 @@ static cudaError_t ws_run(dim3 grid, int nt, size_t smem, const SlideParams& p, 
     return cudaGetLastError();
 }
 
-template <int VO>
+template <int V, int VO>
 static cudaError_t ws_dispatch_vo(int m, bool sv, dim3 grid, int nt, size_t smem,
                                   const SlideParams& p, cudaStream_t st, int* occ) {
 #define DTB_WS_M(M)                                                                          \
     if (p.nseg)                                                                              \
-        return sv ? ws_run<VO, M, DTB_METHOD_SAUVOLA | 4>(grid, nt, smem, p, st, occ)         \
-                  : ws_run<VO, M, DTB_METHOD_NIBLACK | 4>(grid, nt, smem, p, st, occ);        \
-    return sv ? ws_run<VO, M, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ)                 \
-              : ws_run<VO, M, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
+        return sv ? ws_run<V, VO, M, DTB_METHOD_SAUVOLA | 4>(grid, nt, smem, p, st, occ)      \
+                  : ws_run<V, VO, M, DTB_METHOD_NIBLACK | 4>(grid, nt, smem, p, st, occ);     \
+    return sv ? ws_run<V, VO, M, DTB_METHOD_SAUVOLA>(grid, nt, smem, p, st, occ)              \
+              : ws_run<V, VO, M, DTB_METHOD_NIBLACK>(grid, nt, smem, p, st, occ);
     switch (m) {
         case 0: { DTB_WS_M(0) }
         case 1: { DTB_WS_M(1) }
@@ -1204,12 +1213,17 @@ static cudaError_t ws_dispatch_vo(int m, bool sv, dim3 grid, int nt, size_t smem
 #undef DTB_WS_M
 }
 
-// outputs per output thread: 32 (16 measured slower on B200 and is not exposed)
-static int ws_vo() { return 32; }
+// V = VO = 16 variant (DTB_WS_V16=1): half the per-thread state, twice the warps
+static int ws_v16() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("DTB_WS_V16"); v = e ? atoi(e) : DTB_WS_V16_DEFAULT; }
+    return v;
+}
 
 static cudaError_t ws_dispatch(int m, bool sv, dim3 grid, int nt, size_t smem, const SlideParams& p,
-                               cudaStream_t st, int* occ) {
-    return ws_dispatch_vo<32>(m, sv, grid, nt, smem, p, st, occ);
+                               cudaStream_t st, int* occ, bool v16) {
+    if (v16) return ws_dispatch_vo<16, 16>(m, sv, grid, nt, smem, p, st, occ);
+    return ws_dispatch_vo<32, 32>(m, sv, grid, nt, smem, p, st, occ);
 }
 
 static int use_ws() {
@@ -1259,8 +1273,10 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // ms; single-column-warp strips such as C3's are faster on the classic kernel)
     const int ws_mode = use_ws();
     if (V == 32 && (ws_mode == 1 || (ws_mode == 2 && best_w >= 2))) {
-        p.ncw = best_w;
-        p.now = (best_tw + 32 * ws_vo() - 1) / (32 * ws_vo());
+        const bool v16 = ws_v16() && best_w <= 4;  // column-warp totals table holds 8 warps
+        const int vo = v16 ? 16 : 32;
+        p.ncw = v16 ? 2 * best_w : best_w;
+        p.now = (best_tw + 32 * vo - 1) / (32 * vo);
         {
             static int swap_mode = -1;
             if (swap_mode < 0) {
@@ -1276,7 +1292,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         const int m = p.rx & 3;
         const bool sv = p.method == DTB_METHOD_SAUVOLA;
         int occ = 1;
-        ws_dispatch(m, sv, dim3(), nt, smem, p, st, &occ);
+        ws_dispatch(m, sv, dim3(), nt, smem, p, st, &occ, v16);
         const int slots = num_sms * occ;
         int nbands = std::max(1, (int)(band_scale() * slots / std::max(1, best_strips * n_images)));
         nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
@@ -1285,7 +1301,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         if (print_plan())
             fprintf(stderr, "[dtb plan] ws_kernel cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d\n",
                     p.cols, rows_out, p.r, best_w, best_strips, best_tw, occ, (int)grid.y, p.TH);
-        return ws_dispatch(m, sv, grid, nt, smem, p, st, nullptr);
+        return ws_dispatch(m, sv, grid, nt, smem, p, st, nullptr, v16);
     }
     const int nt = 32 * best_w;
     p.NC = V * nt;
