@@ -219,9 +219,18 @@ def run_ours(a):
                                  device=dev) for _ in range(nrot)] if world > 1 and not use_p2p else None
         # p2p: map the neighbours' bands once (CUDA IPC); each step's kernel then reads the
         # halo rows in place over NVLink -- no exchange step.  Bands are constant after setup.
-        peers = [D.PeerHalos(bands[j], w["rows"], r) for j in range(nrot)] if use_p2p else None
+        peers = None
         if use_p2p:
-            peers[0].barrier()
+            try:
+                peers = [D.PeerHalos(bands[j], w["rows"], r) for j in range(nrot)]
+                peers[0].barrier()
+            except (RuntimeError, ValueError) as exc:  # e.g. VMM allocations without IPC handles
+                if rank == 0:
+                    print(f"[bench] p2p halos unavailable ({exc}); using NCCL", file=sys.stderr)
+                use_p2p, peers = False, None
+        if world > 1 and not use_p2p and halo_bufs is None:
+            halo_bufs = [torch.empty((hz - ha,) + tuple(band.shape[1:]), dtype=torch.uint8,
+                                     device=dev) for _ in range(nrot)]
         w["halo_transport"] = ("none (1 GPU)" if world == 1 else
                      "read in place from the neighbours' HBM over NVLink (CUDA IPC), fused into "
                      "the kernel's row staging" if use_p2p else "NCCL send/recv copy per step")
