@@ -16,6 +16,8 @@ Writes (all committed; nothing here reads /root/reference at test time):
 * metrics.npz    -- evaluate() counts/ratios on random bi-level pairs and full sweep()
                     grids (cells + best) on gen_synthetic pages (§8 row f2).
 * otsu.npz       -- images + the reference's otsu_threshold T (§8 row f3).
+* acceptance.npz -- the reference acceptance suite's AC5 corpus with its Otsu F-measure and
+                    best (W, k, FM) sweep cells for the naive engine and gs1..gs6.
 * configs.json   -- per BASELINE config: sha256 of the generated input and of
                     the reference's binary output (and tmap for c1/c5), at
                     FULL size.  c4 takes ~90 s and ~21 GB RSS.
@@ -277,10 +279,30 @@ def make_otsu(rng):
     print(f"otsu.npz: {len(ts)} images")
 
 
+def make_acceptance():
+    """acceptance.npz: the reference acceptance suite's AC5 corpus (synthetic_corpus(10)) with
+    the reference's Otsu F-measure and best sweep cells (naive engine and each GS structure,
+    default grids) per page (test_acceptance.py:165-199)."""
+    from docthresh.bench import synthetic_corpus
+    out, meta = {}, []
+    for i, (img, gt) in enumerate(synthetic_corpus(10)):
+        out[f"img{i}"], out[f"gt{i}"] = img, gt
+        otsu_fm = ref.evaluate(ref.apply_global(img, ref.otsu_threshold(img)), gt).f_measure
+        naive = ref.sweep(img, gt, method="sauvola", engine="naive").best
+        gs = {}
+        for st in STRUCTS:
+            b = ref.sweep(img, gt, method="sauvola", engine="sampled", mask=st).best
+            gs[st] = [b.w, b.k, b.f_measure]
+        meta.append({"otsu_fm": otsu_fm, "naive": [naive.w, naive.k, naive.f_measure], "gs": gs})
+        print(f"acceptance page {i}", flush=True)
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(os.path.join(HERE, "acceptance.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-big", action="store_true")
-    ap.add_argument("--only", choices=["small", "to_gray", "configs", "sampled", "metrics", "otsu"])
+    ap.add_argument("--only", choices=["small", "to_gray", "configs", "sampled", "metrics", "otsu", "acceptance"])
     a = ap.parse_args()
     rng = np.random.default_rng(20261019)
     if a.only in (None, "small"):
@@ -293,6 +315,8 @@ def main():
         make_metrics(np.random.default_rng(20261021))
     if a.only in (None, "otsu"):
         make_otsu(np.random.default_rng(20261022))
+    if a.only in (None, "acceptance"):
+        make_acceptance()
     if a.only in (None, "configs"):
         make_configs(a.skip_big)
 

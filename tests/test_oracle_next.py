@@ -56,3 +56,21 @@ def test_otsu_oracle_matches_reference():
     from conftest import load_otsu
     for img, t in load_otsu():
         assert numpy_ref.otsu_threshold(img) == t
+
+
+def test_sweep_oracle_matches_reference_acceptance_corpus():
+    """The AC5 corpus (tests/golden/acceptance.npz): oracle sweep bests == the reference's."""
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_1210_3165_b200.metrics import DEFAULT_K_GRID, DEFAULT_W_GRID
+    z = np.load(os.path.join(GOLDEN, "acceptance.npz"))
+    meta = json.loads(str(z["meta"]))
+    for i in (0, 7):
+        img, gt = z[f"img{i}"], z[f"gt{i}"]
+        _, best = numpy_ref.sweep(img, gt, "sauvola", "naive", "gs3", DEFAULT_W_GRID, DEFAULT_K_GRID)
+        assert list(best) == meta[i]["naive"]
+        _, best = numpy_ref.sweep(img, gt, "sauvola", "sampled", "gs5", DEFAULT_W_GRID, DEFAULT_K_GRID)
+        assert list(best) == meta[i]["gs"]["gs5"]
+        t = numpy_ref.otsu_threshold(img)
+        assert numpy_ref.evaluate_counts(np.where(img < t, 0, 255), gt)[6] == meta[i]["otsu_fm"]
