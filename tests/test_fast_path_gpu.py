@@ -82,3 +82,24 @@ def test_batch_matches_single():
     for i in range(5):
         assert np.array_equal(out[i].cpu().numpy(),
                               oracle.binarize(imgs[i], 31, "niblack", -0.2, tmap=False)[0])
+
+
+@pytest.mark.parametrize("method,k,r", [("sauvola", 1e-6, 128.0), ("sauvola", 0.99, 128.0),
+                                        ("sauvola", 5.0, 128.0), ("sauvola", 0.34, 1.0),
+                                        ("sauvola", 50.0, 2.0), ("sauvola", 0.5, 1e6),
+                                        ("niblack", -5.0, 128.0), ("niblack", 5.0, 128.0),
+                                        ("niblack", 1e-9, 128.0), ("niblack", -0.2, 128.0)])
+@pytest.mark.parametrize("win", [3, 31, 255])
+def test_extreme_parameters_match_oracle(method, k, r, win):
+    """The certified fp32 decision's tolerance scales with k and R: extreme values only make
+    more pixels take the fp64 replay, never a wrong byte."""
+    import torch
+    img = workloads.doc_gray(300, 1100, 13, 150)
+    b, _ = engine.binarize(torch.from_numpy(img).cuda(), win, method, k, r, want_tmap=False)
+    ob = oracle.binarize(img, win, method, k, r, tmap=False, threads=8)[0]
+    assert np.array_equal(b.cpu().numpy(), ob)
+    # and the wide-strip (warp-specialised) kernel on a page wide enough for it
+    wide = workloads.doc_gray(160, 3840, 17, 150)
+    b, _ = engine.binarize(torch.from_numpy(wide).cuda(), win, method, k, r, want_tmap=False)
+    assert np.array_equal(b.cpu().numpy(), oracle.binarize(wide, win, method, k, r, tmap=False,
+                                                           threads=8)[0])
