@@ -50,6 +50,7 @@ SIGNATURES = {
     "dtb_ipc_close": [_c_p],
     "dtb_gs_band": [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
                     _c_p, _c_i64, _c_i32, _c_f64, _c_f64, _c_p],
+    "dtb_set_fp32_audit": [_c_p],
     "dtb_confusion": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
     "dtb_sweep_counts": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p,
                          _c_i32, _c_i32, _c_f64, _c_p, _c_p],

@@ -22,6 +22,7 @@
 namespace dtb {
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st);
 bool slide_ok(int r, int cols, int rows, const void* base, int64_t pitch, int64_t stride);
+cudaError_t set_fp32_audit(unsigned long long* counters);
 }  // namespace dtb
 
 using namespace dtb;
@@ -89,6 +90,11 @@ int dtb_binarize_segments(const uint8_t* const* seg_ptr, const int64_t* seg_pitc
     q.rr = r;
     const cudaError_t e = launch_slide(q, 1, num_sms(), (cudaStream_t)stream);
     return e == cudaSuccess ? DTB_OK : cuda_fail(e, "slide kernel launch (segments)");
+}
+
+int dtb_set_fp32_audit(uint64_t* counters3) {
+    const cudaError_t e = set_fp32_audit(reinterpret_cast<unsigned long long*>(counters3));
+    return e == cudaSuccess ? DTB_OK : cuda_fail(e, "dtb_set_fp32_audit");
 }
 
 int dtb_ipc_export(const void* ptr, uint8_t* handle64, int64_t* offset) {

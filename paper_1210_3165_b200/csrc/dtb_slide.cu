@@ -142,6 +142,11 @@ __device__ __forceinline__ const uint8_t* row_at(const SlideParams& p, const uin
     return p.seg_ptr[i] + (int64_t)(g - p.seg_lo[i]) * p.seg_pitch[i];
 }
 
+// fp32-epilogue audit (dtb_set_fp32_audit): when set, the replay path counts
+// [0] pixels replayed in fp64 (|f - t32| < tol), [1] pixels whose plain fp32 sign would have
+// flipped the reference's decision, [2] max |f - t_fp64| over those (float bits).
+__device__ unsigned long long* g_fp32_audit = nullptr;
+
 // Rare path, out of line: re-decide this thread's 32 pixels, the uncertain ones (|f - t32| < tol)
 // with the reference fp64 sequence.  S/Q are read back from the shared prefix (valid until the next
 // row's first barrier); corrected bytes are written after the vector stores (program order).
@@ -165,8 +170,22 @@ __device__ __noinline__ void fix_uncertain(const uint32_t* sPS, const uint32_t* 
                                  : fast_diff<METHOD, true>(S, Q, f, n, cA, cC, a, c);
         // rewrite every pixel of the thread: the caller's decision may have used the other
         // (border) constant set, so its certified set can differ from this one's
-        orow[x] = (fabsf(d) >= tol) ? (d < 0.f ? 0 : 255)
-                                    : (uint8_t)exact_white(S, Q, (double)n, f, METHOD, k, rr);
+        if (fabsf(d) >= tol) {
+            orow[x] = d < 0.f ? 0 : 255;
+            continue;
+        }
+        const uint32_t white = exact_white(S, Q, (double)n, f, METHOD, k, rr);
+        orow[x] = (uint8_t)white;
+        if (unsigned long long* audit = g_fp32_audit) {
+            atomicAdd(&audit[0], 1ull);
+            if (white != (d < 0.f ? 0u : 0xFFu)) {
+                double mean, sd;
+                finish_exact((double)S, (double)Q, (double)n, mean, sd);
+                const float gap = (float)fabs((double)f - threshold_exact(mean, sd, METHOD, k, rr));
+                atomicAdd(&audit[1], 1ull);
+                atomicMax(&audit[2], (unsigned long long)__float_as_uint(gap));
+            }
+        }
     }
 }
 
@@ -1246,6 +1265,10 @@ static double band_scale() {
     static double v = -1.0;
     if (v < 0) { const char* e = getenv("DTB_BAND_SCALE"); v = e ? atof(e) : 1.0; if (!(v > 0)) v = 1.0; }
     return v;
+}
+
+cudaError_t set_fp32_audit(unsigned long long* counters) {
+    return cudaMemcpyToSymbol(g_fp32_audit, &counters, sizeof(counters));
 }
 
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
