@@ -51,6 +51,7 @@ SIGNATURES = {
     "dtb_gs_band": [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32,
                     _c_p, _c_i64, _c_i32, _c_f64, _c_f64, _c_p],
     "dtb_set_fp32_audit": [_c_p],
+    "dtb_last_kernel": [],
     "dtb_confusion": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
     "dtb_sweep_counts": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p,
                          _c_i32, _c_i32, _c_f64, _c_p, _c_p],
@@ -78,7 +79,8 @@ def lib():
             continue
         fn = getattr(L, name)
         fn.argtypes = argtypes
-        fn.restype = ctypes.c_char_p if name == "dtb_last_error" else ctypes.c_int
+        fn.restype = (ctypes.c_char_p if name in ("dtb_last_error", "dtb_last_kernel")
+                      else ctypes.c_int)
     _lib = L
     return L
 

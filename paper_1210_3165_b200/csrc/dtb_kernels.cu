@@ -365,6 +365,7 @@ static cudaError_t run_strip(dim3 grid, const StripParams& p, cudaStream_t st) {
 
 template <int MODE>
 static int launch_strip(StripParams p, int n_images, cudaStream_t st) {
+    if (MODE == MODE_BINARIZE) set_last_kernel("strip_kernel");
     constexpr int NT = 256;
     const int rows_out = p.out_end - p.out_begin;
     if (rows_out <= 0 || p.cols <= 0 || n_images <= 0) return DTB_OK;

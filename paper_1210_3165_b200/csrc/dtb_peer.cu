@@ -92,6 +92,8 @@ int dtb_binarize_segments(const uint8_t* const* seg_ptr, const int64_t* seg_pitc
     return e == cudaSuccess ? DTB_OK : cuda_fail(e, "slide kernel launch (segments)");
 }
 
+const char* dtb_last_kernel(void) { return dtb::last_kernel(); }
+
 int dtb_set_fp32_audit(uint64_t* counters3) {
     const cudaError_t e = set_fp32_audit(reinterpret_cast<unsigned long long*>(counters3));
     return e == cudaSuccess ? DTB_OK : cuda_fail(e, "dtb_set_fp32_audit");

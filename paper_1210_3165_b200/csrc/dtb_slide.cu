@@ -1084,6 +1084,482 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
     }
 }
 
+// =====================================================================================
+// Group-bound kernel (gb_kernel, Sauvola with 0 < k <= 1).  Warp-specialised like ws_kernel
+// (same ring, same READY/FREE hand-off), with a leaner column phase and a different output
+// phase:
+//
+// * Residue-decimated prefix layout.  Word k of a prefix array (k in [0, NC]; word k = sum of
+//   strip columns [0, k)) lives in plane rho = k & 3 at dec index m = k >> 2.  Dec index m
+//   belongs to column lane t = m >> 3, half hh = (m >> 2) & 1, element m & 3, stored at
+//   plane + 4*(hh*(T+1) + t) + (m & 3) (T column lanes).  A column lane writes its 32 words
+//   as 8 STS.128 (two per plane) and an output lane reads every 4th word of a run -- the only
+//   words the group bounds need -- as 2-3 LDS.128 per stream.  Both are bank-conflict free.
+//
+// * Group bounds.  For 4 adjacent outputs x0..x0+3 the window sums satisfy, because the
+//   column sums are >= 0 (prefix words are nondecreasing),
+//       S_I <= S(x) <= S_U,   Q(x) <= Q_U
+//   with I = [x0+3-r, x0+r] (intersection of the 4 windows) and U = [x0-r, x0+3+r] (union):
+//       S_U = P[b+3] - P[a],  S_I = P[b] - P[a+3],  Q_U = PQ[b+3] - PQ[a]   (a, b: run starts).
+//   Sauvola's t = m (1-k) + (k/R) m s is nondecreasing in s and, for 0 <= 1-k, in m, so
+//       t_lo = m_lo (1-k) <= t <= t_hi = m_hi ((1-k) + (k/R) sqrt(Q_U/n_lo - m_lo^2))
+//   (m_lo = S_I/n_hi, m_hi = S_U/n_lo; n_lo..n_hi the pixels' counts).  Evaluated in fp32
+//   with directed slack (relative 2^-17 on every factor, 1e-4 absolute) the bounds also
+//   enclose the reference's fp64 threshold.  A pixel with f < ceil(t_lo) is black, one with
+//   f >= ceil(t_hi) is white (f is an integer); the compare runs on 16-bit SWAR lanes, four
+//   pixels per handful of instructions.  Pixels in [ceil(t_lo), ceil(t_hi)) are uncertain:
+//   their group is re-decided per pixel (exact S, Q from the prefix -> certified fp32 ->
+//   fp64 replay), out of line.  On document pages this is ~1e-5 of the groups at W=127.
+// =====================================================================================
+#ifndef GB_STAGES
+#define GB_STAGES 5
+#endif
+#ifndef DTB_GB_MAXREG
+#define DTB_GB_MAXREG 168
+#endif
+
+#define GB_NC 2048
+// words of one residue plane: 2 rows of (T+1) chunks
+__host__ __device__ constexpr int gb_plane_words(int NC) { return 8 * (NC / 32 + 1); }
+
+__host__ __device__ inline size_t gb_smem_bytes(int NC) {
+    // 2 buffers x (S, Q) x 4 planes, warp totals, 2*NS mbarriers, NS stages x 3 row segments
+    return sizeof(uint32_t) * (16 * (size_t)gb_plane_words(NC) + 32) + 2 * GB_STAGES * sizeof(uint64_t) +
+           (size_t)GB_STAGES * 3 * NC;
+}
+
+// word k of a residue-decimated prefix array (rare paths only)
+__device__ __forceinline__ uint32_t gb_word(const uint32_t* arr, int PW, int T1, int k) {
+    const int m = k >> 2;
+    return arr[(k & 3) * PW + 4 * (((m >> 2) & 1) * T1 + (m >> 3)) + (m & 3)];
+}
+
+// 8 consecutive dec words m0..m0+7 of one plane, m0 = 8*t0 + D (D compile-time, 0..7)
+template <int D>
+__device__ __forceinline__ void gb_stream(const uint32_t* plane, int t0, int T1, uint32_t (&w)[8]) {
+    constexpr int MU = D & 3;
+    const uint32_t* c0 = plane + 4 * ((D < 4 ? 0 : T1) + t0);
+    const uint32_t* c1 = plane + 4 * ((D < 4 ? T1 : 0) + t0 + (D < 4 ? 0 : 1));
+    const uint32_t* c2 = plane + 4 * ((D < 4 ? 0 : T1) + t0 + 1);
+    uint32_t v[12];
+    {
+        const uint4 x = *reinterpret_cast<const uint4*>(c0);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        const uint4 y = *reinterpret_cast<const uint4*>(c1);
+        v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+        if (MU) {
+            const uint4 z = *reinterpret_cast<const uint4*>(c2);
+            v[8] = z.x; v[9] = z.y; v[10] = z.z; v[11] = z.w;
+        } else {
+            v[8] = v[9] = v[10] = v[11] = 0;
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) w[g] = v[MU + g];
+}
+
+// ceil(x) for x in (-0.5, 2^22) as a pair of 16-bit lanes (x, x): FADD.RP onto 2^23 leaves
+// 2^23 + ceil(x), whose bit pattern minus 0x4B000000 is ceil(x); the IMAD replicates it.
+__device__ __forceinline__ uint32_t gb_ceil2(float x) {
+    const uint32_t bits = __float_as_uint(__fadd_ru(x, 8388608.0f));
+    return bits * 0x10001u - 0x4B000000u * 0x10001u;
+}
+
+// Uncertain group of 4 pixels (gb_kernel), out of line: exact S, Q per pixel from the
+// residue-decimated prefix, certified fp32 decision, reference fp64 replay when within tol.
+__device__ __noinline__ void gb_fix_group(const uint32_t* sPS, const uint32_t* sPQ, int PW, int T1,
+                                          int a_word, int b_word, const uint8_t* f4, uint8_t* orow,
+                                          int x0, int cols, int ny, int r, float cA, float cC,
+                                          float ca, float cc, float tol, double kk, double rr) {
+    for (int i = 0; i < 4; ++i) {
+        const int x = x0 + i;
+        if (x >= cols) break;
+        const uint32_t S = gb_word(sPS, PW, T1, b_word + i) - gb_word(sPS, PW, T1, a_word + i);
+        const uint32_t Q = gb_word(sPQ, PW, T1, b_word + i) - gb_word(sPQ, PW, T1, a_word + i);
+        const uint32_t f = f4[i];
+        const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
+        const uint32_t n = (uint32_t)(ny * nx);
+        const float d = fast_diff<DTB_METHOD_SAUVOLA, true>(S, Q, f, n, cA, cC, ca, cc);
+        uint32_t white;
+        if (fabsf(d) >= tol) {
+            white = d < 0.f ? 0u : 0xFFu;
+        } else {
+            white = exact_white(S, Q, (double)n, f, DTB_METHOD_SAUVOLA, kk, rr);
+            if (unsigned long long* audit = g_fp32_audit) {
+                atomicAdd(&audit[0], 1ull);
+                if (white != (d < 0.f ? 0u : 0xFFu)) atomicAdd(&audit[1], 1ull);
+            }
+        }
+        orow[x] = (uint8_t)white;
+    }
+}
+
+// DTB_GB_TIMES=1 (debug): per-CTA start/end %globaltimer, printed by the launcher.
+__device__ unsigned long long g_gb_times[2 * 8192];
+__device__ int g_gb_times_on = 0;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// R16 = r & 15 (fixes every stream's alignment); interior rows/lanes use n = (2r+1)^2.
+template <int R16>
+__global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
+    constexpr int NS = GB_STAGES;
+    constexpr int ALPHA = (16 - R16) & 15;
+    constexpr int EB = (ALPHA + 2 * R16 + 1) & 31;  // (alpha + 2r + 1) mod 32
+    // compile-time dec offsets (mod 8) of the six streams
+    constexpr int D_A0 = (ALPHA >> 2) & 7, D_A3 = ((ALPHA + 3) >> 2) & 7;
+    constexpr int D_B0 = (EB >> 2) & 7, D_B3 = ((EB + 3) >> 2) & 7;
+    constexpr int R_A0 = ALPHA & 3, R_A3 = (ALPHA + 3) & 3, R_B0 = EB & 3, R_B3 = (EB + 3) & 3;
+    extern __shared__ __align__(128) uint32_t sm[];
+    constexpr int NC = GB_NC;  // 2 column warps (the host launches gb_kernel only with ncw = 2)
+    constexpr int PW = gb_plane_words(NC);
+    constexpr int T = NC / 32, T1 = T + 1;
+    uint32_t* sWS = sm + 16 * PW;  // [2][8] per-column-warp totals, double buffered
+    uint32_t* sWQ = sWS + 16;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sWS + 32);
+    uint64_t* empty = full + NS;
+    uint8_t* ring = reinterpret_cast<uint8_t*>(empty + NS);
+    const int ncw = p.ncw, now = p.now, nthr = 32 * (ncw + now);
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const bool is_col = warp < ncw;
+    const int bid = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+    if (g_gb_times_on && t == 0 && bid < 8192) g_gb_times[2 * bid] = gtimer();
+    const uint8_t* in = p.in + (int64_t)blockIdx.z * p.img_stride;
+    const int X0 = (int)blockIdx.x * p.TW;
+    const int xc0 = X0 - p.r - ALPHA;
+    const int ya = p.out_begin + (int)blockIdx.y * p.TH;
+    const int yb = min(ya + p.TH, p.out_end);
+    if (ya >= yb) return;
+    const uint8_t* in0 = in - (int64_t)p.row0 * p.pitch;
+    const int c_lo = max(xc0, 0);
+    const int c_hi = min(xc0 + NC, p.cols);
+    const int c_hi16 = c_lo + ((max(c_hi - c_lo, 0)) & ~15);
+    const int f_hi = min(X0 + p.TW, p.cols);
+    const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
+    Items it;
+    it.g0 = max(ya - p.r, 0);
+    it.nwarm = min(ya + p.r, p.H - 1) - it.g0 + 1;
+    it.ya = ya;
+    it.n = it.nwarm + (yb - ya);
+
+    {
+        uint4* r4 = reinterpret_cast<uint4*>(ring);
+        const int n16 = NS * 3 * NC / 16;
+        for (int i = t; i < n16; i += blockDim.x) r4[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], ncw + now);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint64_t pol_keep = make_policy(p.l2hint ? 2 : 0), pol_drop = make_policy(p.l2hint ? 1 : 0);
+    auto issue = [&](int k) {
+        const int s = k % NS;
+        if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
+        uint8_t* E = ring + (size_t)s * 3 * NC;
+        uint8_t* O = E + NC;
+        uint8_t* F = O + NC;
+        int ge, go = -1, gf = -1;
+        if (k < it.nwarm) {
+            ge = it.g0 + k;
+        } else {
+            const int y = it.ya + (k - it.nwarm);
+            gf = y;
+            ge = (k == it.nwarm) ? -1 : y + p.r;
+            go = (k == it.nwarm) ? -1 : y - p.r - 1;
+            if (ge >= p.H) ge = -1;
+        }
+        const uint32_t rowb = (uint32_t)(c_hi16 - c_lo), fb = (uint32_t)(f_hi16 - X0);
+        uint32_t bytes = 0;
+        if (ge >= 0) bytes += rowb;
+        if (go >= 0) bytes += rowb;
+        if (gf >= 0) bytes += fb;
+        mbar_expect_tx(&full[s], bytes);
+        if (ge >= 0 && rowb) bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s], pol_keep);
+        if (go >= 0 && rowb) bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s], pol_drop);
+        if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s], pol_keep);
+        for (int c = c_hi16; c < c_hi; ++c) {
+            if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
+            if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+        }
+        for (int c = f_hi16; c < f_hi; ++c)
+            if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+    };
+
+    // The producer is lane 0 of the first OUTPUT warp: it refills a ring slot once all four
+    // warps released it, so a column warp never blocks on the output warps' progress (a
+    // column-warp producer stalled READY(k) behind output row k-1).
+    const bool producer = (t == 32 * ncw);
+    if (is_col) {
+        // ===================== column warps =====================
+        uint32_t cS[32], cQ[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { cS[j] = 0; cQ[j] = 0; }
+        for (int k = 0; k < it.nwarm; ++k) {
+            const int s = k % NS;
+            mbar_wait(&full[s], (k / NS) & 1);
+            const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * NC + 32 * t);
+            uint32_t w[8];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint4 a = E[q];
+                w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t v = byte_at(w, j);
+                cS[j] += v;
+                cQ[j] += v * v;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cnt(&empty[s], warp == 0 ? 1 + now : 1);
+        }
+
+        for (int k = it.nwarm; k < it.n; ++k) {
+            const int y = it.ya + (k - it.nwarm);
+            const int s = k % NS;
+            const int b = (k - it.nwarm) & 1;
+            mbar_wait(&full[s], (k / NS) & 1);
+            const uint8_t* stage = ring + (size_t)s * 3 * NC;
+            const bool first = (k == it.nwarm);
+            const bool ein = !first && y + p.r < p.H, oin = !first && y - p.r - 1 >= 0;
+            if (ein && oin) {
+                uint32_t e[8], o[8];
+                const uint4* E = reinterpret_cast<const uint4*>(stage + 32 * t);
+                const uint4* O = reinterpret_cast<const uint4*>(stage + NC + 32 * t);
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const uint4 a = E[q], bb = O[q];
+                    e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
+                    o[4 * q] = bb.x; o[4 * q + 1] = bb.y; o[4 * q + 2] = bb.z; o[4 * q + 3] = bb.w;
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
+                    cS[j] = cS[j] + ev - ov;
+                    cQ[j] = cQ[j] + ev * ev - ov * ov;
+                }
+            } else if (ein || oin) {
+                // image top / bottom: one of the two rows is outside the image
+                uint32_t e[8];
+                const uint4* E = reinterpret_cast<const uint4*>(stage + (ein ? 0 : NC) + 32 * t);
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const uint4 a = E[q];
+                    e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
+                }
+                const uint32_t sg = ein ? 1u : 0xFFFFFFFFu;  // +1 entering, -1 leaving
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t ev = byte_at(e, j);
+                    cS[j] += sg * ev;
+                    cQ[j] += sg * (ev * ev);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with item k's rows
+            // quarter sums (tree) -> lane total -> warp scan -> cross-warp totals
+            uint32_t qS[4], qQ[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int c = 8 * h;
+                qS[h] = ((cS[c] + cS[c + 1]) + (cS[c + 2] + cS[c + 3])) + ((cS[c + 4] + cS[c + 5]) + (cS[c + 6] + cS[c + 7]));
+                qQ[h] = ((cQ[c] + cQ[c + 1]) + (cQ[c + 2] + cQ[c + 3])) + ((cQ[c + 4] + cQ[c + 5]) + (cQ[c + 6] + cQ[c + 7]));
+            }
+            const uint32_t TS = (qS[0] + qS[1]) + (qS[2] + qS[3]);
+            const uint32_t TQ = (qQ[0] + qQ[1]) + (qQ[2] + qQ[3]);
+            uint32_t iS = TS, iQ = TQ;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
+                const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
+                if (lane >= off) { iS += vs; iQ += vq; }
+            }
+            if (lane == 31) { sWS[8 * b + warp] = iS; sWQ[8 * b + warp] = iQ; }
+            nbar_sync(BAR_COLS, 32 * ncw);
+            uint32_t bS = iS - TS, bQ = iQ - TQ;
+            for (int w = 0; w < warp; ++w) { bS += sWS[8 * b + w]; bQ += sWQ[8 * b + w]; }
+            // wait until the output warps have consumed row k-2 from this prefix buffer
+            nbar_sync(BAR_FREE0 + b, nthr);
+            uint32_t* sPS = sm + (2 * b) * 4 * PW + 4 * t;
+            uint32_t* sPQ = sPS + 4 * PW;
+            // exclusive running prefix, stored residue-decimated: half hh of the lane's columns
+            // (two quarter chains) -> plane rho chunk (hh, t) = {pre[16hh+rho+4i], i = 0..3}
+            {
+                uint32_t cb0S = bS, cb0Q = bQ;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    uint32_t c1S = cb0S + qS[2 * hh], c1Q = cb0Q + qQ[2 * hh];
+                    uint32_t vS[4][4], vQ[4][4];  // [rho][i]
+                    uint32_t r0S = cb0S, r0Q = cb0Q, r1S = c1S, r1Q = c1Q;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int j0 = 16 * hh + i, j1 = j0 + 8;
+                        vS[i & 3][i >> 2] = r0S; vQ[i & 3][i >> 2] = r0Q;
+                        vS[i & 3][2 + (i >> 2)] = r1S; vQ[i & 3][2 + (i >> 2)] = r1Q;
+                        r0S += cS[j0]; r0Q += cQ[j0];
+                        r1S += cS[j1]; r1Q += cQ[j1];
+                    }
+#pragma unroll
+                    for (int rho = 0; rho < 4; ++rho) {
+                        const int pos = rho * PW + 4 * hh * T1;
+                        *reinterpret_cast<uint4*>(&sPS[pos]) = make_uint4(vS[rho][0], vS[rho][1], vS[rho][2], vS[rho][3]);
+                        *reinterpret_cast<uint4*>(&sPQ[pos]) = make_uint4(vQ[rho][0], vQ[rho][1], vQ[rho][2], vQ[rho][3]);
+                    }
+                    cb0S = c1S + qS[2 * hh + 1]; cb0Q = c1Q + qQ[2 * hh + 1];
+                }
+                if (t == 32 * ncw - 1) {  // word NC: plane 0, dec index 8T -> chunk (0, T)
+                    sPS[4] = cb0S;
+                    sPQ[4] = cb0Q;
+                }
+            }
+            nbar_arrive(BAR_READY0 + b, nthr);
+        }
+        const int rows = it.n - it.nwarm;
+        if (rows >= 1) nbar_sync(BAR_FREE0 + (rows & 1), nthr);
+        if (rows >= 2) nbar_sync(BAR_FREE0 + ((rows + 1) & 1), nthr);
+    } else {
+        // ===================== output warps =====================
+        const int to = t - 32 * ncw;
+        const int xo = X0 + 32 * to;
+        const bool has_out = (32 * to + 32 + 2 * p.r + ALPHA <= NC) && (32 * to < p.TW) && (xo < p.cols);
+        const bool out_full = has_out && (xo + 32 <= p.cols) &&
+                              ((reinterpret_cast<uintptr_t>(p.bin) | (uintptr_t)p.bin_pitch |
+                                (uintptr_t)p.out_stride) & 15) == 0;
+        const bool x_interior = (xo - p.r >= 0) && (xo + 31 + p.r <= p.cols - 1);
+        const bool border_warp = __any_sync(0xffffffffu, has_out && !x_interior);
+        const int qB = (ALPHA + 2 * p.r + 1) >> 5;  // lane offset of the B streams
+        const int qB3 = (ALPHA + 2 * p.r + 4) >> 5;
+        const int a_word = ALPHA + 32 * to, b_word = ALPHA + 2 * p.r + 1 + 32 * to;
+        const float W = (float)(2 * p.r + 1);
+        const float a1 = p.a, cK = p.c;  // 1-k, k/R
+        const float kUp = 1.0f + 7.62939453125e-6f, kDn = 1.0f - 7.62939453125e-6f;  // 1 +- 2^-17
+        const float dAbs = p.tol;  // >= the reference's own fp64 error on t (slide_constants)
+        uint8_t* obase = p.bin + (int64_t)blockIdx.z * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
+        nbar_arrive(BAR_FREE0, nthr);  // both prefix buffers start free
+        nbar_arrive(BAR_FREE0 + 1, nthr);
+        int issued = 0;
+        if (producer) {  // the ring's first NS items, then every warm-up slot as it frees up
+            while (issued < min(NS, it.n)) issue(issued++);
+            while (issued < min(it.nwarm + NS - 1, it.n)) issue(issued++);
+        }
+        for (int k = it.nwarm; k < it.n; ++k) {
+            const int y = it.ya + (k - it.nwarm);
+            const int s = k % NS;
+            const int b = (k - it.nwarm) & 1;
+            nbar_sync(BAR_READY0 + b, nthr);
+            // every warp released item k-1 by now (output warps: program order before READY(k);
+            // column warps: before READY(k-1)), so refilling its slot never blocks
+            if (producer)
+                while (issued < min(k + NS, it.n)) issue(issued++);
+            mbar_wait(&full[s], (k / NS) & 1);  // (complete; makes the staged rows visible)
+            const uint8_t* stage = ring + (size_t)s * 3 * NC;
+            const uint32_t* sPS = sm + (2 * b) * 4 * PW;
+            const uint32_t* sPQ = sPS + 4 * PW;
+            if (has_out) {
+                uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
+                const int ny = min(y + p.r, p.H - 1) - max(y - p.r, 0) + 1;
+                const uint8_t* fsm = stage + 2 * NC + 32 * to;
+                uint32_t fw[8];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(fsm + 16 * q);
+                    fw[4 * q] = v.x; fw[4 * q + 1] = v.y; fw[4 * q + 2] = v.z; fw[4 * q + 3] = v.w;
+                }
+                uint32_t SA0[8], SA3[8], SB0[8], SB3[8], QA0[8], QB3[8];
+                gb_stream<D_A0>(sPS + R_A0 * PW, to, T1, SA0);
+                gb_stream<D_A3>(sPS + R_A3 * PW, to, T1, SA3);
+                gb_stream<D_B0>(sPS + R_B0 * PW, to + qB, T1, SB0);
+                gb_stream<D_B3>(sPS + R_B3 * PW, to + qB3, T1, SB3);
+                gb_stream<D_A0>(sPQ + R_A0 * PW, to, T1, QA0);
+                gb_stream<D_B3>(sPQ + R_B3 * PW, to + qB3, T1, QB3);
+                // 1/n for the row (interior lanes: n = ny * W for every pixel), with the slack
+                const float rnr = rcp_ftz((float)ny * W);  // rel. error << the 2^-17 slack
+                const float rloR = rnr * kUp, rhiR = rnr * kDn;
+                uint32_t ow[8];
+                uint32_t um = 0;  // groups with an uncertain pixel
+                auto group = [&](int g, float rlo, float rhi) {
+                    const uint32_t SU = SB3[g] - SA0[g];
+                    const uint32_t SI = SB0[g] - SA3[g];
+                    const uint32_t QU = QB3[g] - QA0[g];
+                    const float mhi = (float)SU * rlo;
+                    const float mlo = (float)SI * rhi;
+                    const float v = __fmaf_rn((float)QU, rlo, -(mlo * mlo));
+                    const float sd = sqrt_ftz(fmaxf(v, 0.f));
+                    const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sd, cK, a1), dAbs), 4096.f);
+                    const float tlo = __fmaf_rn(mlo, a1, -dAbs);
+                    const uint32_t H2 = gb_ceil2(thi), L2 = gb_ceil2(tlo);
+                    // SWAR: 16-bit lanes (f | 0x8000) - T: bit 15 set iff f >= T
+                    const uint32_t f4 = fw[g];
+                    const uint32_t fA = prmt(f4, 0x80808080u, 0x4240);  // pixels 0, 2
+                    const uint32_t fB = prmt(f4, 0x80808080u, 0x4341);  // pixels 1, 3
+                    const uint32_t wA = fA - H2, wB = fB - H2;
+                    ow[g] = prmt(wA, wB, 0xFBD9);  // bytes 0xFF where f >= ceil(t_hi)
+                    const uint32_t u = ((fA - L2) & ~wA) | ((fB - L2) & ~wB);
+                    if (u & 0x80008000u) um |= 1u << g;
+                };
+                if (!border_warp) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) group(g, rloR, rhiR);
+                } else {
+                    // a warp with image-edge lanes: every lane takes per-group counts (warp-uniform)
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        int nmin = 1 << 30, nmax = 0;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int x = xo + 4 * g + i;
+                            const int nx = min(x + p.r, p.cols - 1) - max(x - p.r, 0) + 1;
+                            nmin = min(nmin, nx); nmax = max(nmax, nx);
+                        }
+                        nmin = max(nmin, 1);
+                        group(g, rcp_ftz((float)(ny * nmin)) * kUp, rcp_ftz((float)(ny * nmax)) * kDn);
+                    }
+                }
+                if (out_full) {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        __stcs(reinterpret_cast<uint4*>(orow + xo + 16 * q),
+                               make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int x = xo + j;
+                        if (x < p.cols) orow[x] = (uint8_t)(ow[j >> 2] >> (8 * (j & 3)));
+                    }
+                }
+                // Uncertain groups, out of line and after the vector stores (program order): each
+                // round, every lane with a flagged group re-decides one of them per pixel.
+                const unsigned am = __activemask();  // the lanes with outputs
+                while (__builtin_expect(__any_sync(am, um != 0u), 0)) {
+                    if (um) {
+                        const int g = __ffs(um) - 1;
+                        um &= um - 1;
+                        gb_fix_group(sPS, sPQ, PW, T1, ALPHA + 32 * to + 4 * g,
+                                     ALPHA + 2 * p.r + 1 + 32 * to + 4 * g, fsm + 4 * g, orow,
+                                     xo + 4 * g, p.cols, ny, p.r, p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            nbar_arrive(BAR_FREE0 + b, nthr);
+        }
+    }
+    if (g_gb_times_on && bid < 8192) {
+        __syncthreads();
+        if (t == 0) g_gb_times[2 * bid + 1] = gtimer();
+    }
+}
+
 // Certified tolerance (see header comment):  |t_fp32 - t_exact| <= E_fast and
 // |t_reference - t_exact| <= E_ref, so |f - t_fp32| >= tol = 2 (E_fast + E_ref) fixes the sign of
 // f - t_reference.  E_ref: the reference's var = Q/n - mean^2 carries <= 5u Q/n <= 3.6e-11
@@ -1267,6 +1743,64 @@ static double band_scale() {
     return v;
 }
 
+// ---- group-bound launcher (gb_kernel)
+template <int R16>
+static cudaError_t gb_run(dim3 grid, int nt, size_t smem, const SlideParams& p, cudaStream_t st,
+                          int* occ) {
+    static size_t granted = 48 * 1024;
+    auto kern = gb_kernel<R16>;
+    if (smem > granted) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        granted = smem;
+    }
+    if (occ) {
+        static int c_nt[16], c_occ[16];
+        static size_t c_smem[16];
+        static int nc = 0;
+        for (int i = 0; i < nc; ++i)
+            if (c_nt[i] == nt && c_smem[i] == smem) { *occ = c_occ[i]; return cudaSuccess; }
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nt, smem) != cudaSuccess)
+            blocks = 1;
+        *occ = std::max(blocks, 1);
+        if (nc < 16) { c_nt[nc] = nt; c_smem[nc] = smem; c_occ[nc] = *occ; ++nc; }
+        return cudaSuccess;
+    }
+    kern<<<grid, nt, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+static cudaError_t gb_dispatch(int r16, dim3 grid, int nt, size_t smem, const SlideParams& p,
+                               cudaStream_t st, int* occ) {
+    switch (r16) {
+#define DTB_GB_CASE(R) case R: return gb_run<R>(grid, nt, smem, p, st, occ);
+        DTB_GB_CASE(0) DTB_GB_CASE(1) DTB_GB_CASE(2) DTB_GB_CASE(3)
+        DTB_GB_CASE(4) DTB_GB_CASE(5) DTB_GB_CASE(6) DTB_GB_CASE(7)
+        DTB_GB_CASE(8) DTB_GB_CASE(9) DTB_GB_CASE(10) DTB_GB_CASE(11)
+        DTB_GB_CASE(12) DTB_GB_CASE(13) DTB_GB_CASE(14) DTB_GB_CASE(15)
+#undef DTB_GB_CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+// DTB_GB: 0 never, 1 whenever eligible, 2 (default) eligible and r >= DTB_GB_MIN_R.
+#ifndef DTB_GB_MIN_R
+#define DTB_GB_MIN_R 31
+#endif
+#ifndef DTB_GB_MIN_COLS
+#define DTB_GB_MIN_COLS 1536
+#endif
+static int gb_mode() {  // read per launch (tests switch it)
+    const char* e = getenv("DTB_GB");
+    return e ? atoi(e) : 2;
+}
+
+static thread_local const char* g_last_kernel = "";
+const char* last_kernel() { return g_last_kernel; }
+void set_last_kernel(const char* name) { g_last_kernel = name; }
+
 cudaError_t set_fp32_audit(unsigned long long* counters) {
     return cudaMemcpyToSymbol(g_fp32_audit, &counters, sizeof(counters));
 }
@@ -1292,6 +1826,58 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         }
     }
     if (best_w == 0) return cudaErrorInvalidValue;  // window too wide for 8 warps (caller checks)
+    // group-bound kernel: Sauvola with 0 < k <= 1, strips of 2 column warps (see gb_kernel)
+    const int gbm = gb_mode();
+    const int gb_tw = 32 * ((GB_NC - 2 * p.rx - alpha) / 32);
+    if (V == 32 && !p.nseg && p.method == DTB_METHOD_SAUVOLA && p.k > 0.0 && p.k <= 1.0 &&
+        p.rx == p.r && gb_tw >= 32 &&
+        (gbm == 1 || (gbm == 2 && p.r >= DTB_GB_MIN_R && p.cols >= DTB_GB_MIN_COLS))) {
+        const int ns = (p.cols + gb_tw - 1) / gb_tw;
+        best_strips = ns;
+        best_tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
+        best_w = GB_NC / 1024;
+        p.ncw = best_w;
+        p.now = (best_tw + 1023) / 1024;
+        p.role_div = 0;
+        p.NC = GB_NC;
+        p.TW = best_tw;
+        const int nt = 32 * (p.ncw + p.now);
+        const size_t smem = gb_smem_bytes(p.NC);
+        int occ = 1;
+        const cudaError_t qe = gb_dispatch(p.r & 15, dim3(), nt, smem, p, st, &occ);
+        if (qe != cudaSuccess) return qe;
+        const int slots = num_sms * occ;
+        // two waves of bands: content-dependent band cost (uncertain groups cluster in dark
+        // page regions) leaves a one-wave launch waiting on its slowest bands (C4: 0.538 vs 0.583 ms)
+        const char* bse = getenv("DTB_BAND_SCALE");
+        const double bscale = bse ? band_scale() : 2.0;
+        int nbands = std::max(1, (int)(bscale * slots / std::max(1, best_strips * n_images)));
+        nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
+        p.TH = (rows_out + nbands - 1) / nbands;
+        dim3 grid(best_strips, (rows_out + p.TH - 1) / p.TH, n_images);
+        if (print_plan())
+            fprintf(stderr, "[dtb plan] gb_kernel cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d smem=%zu\n",
+                    p.cols, rows_out, p.r, best_w, best_strips, best_tw, occ, (int)grid.y, p.TH, smem);
+        g_last_kernel = "gb_kernel";
+        const char* tenv = getenv("DTB_GB_TIMES");
+        if (tenv && tenv[0] == '1') {
+            const int on = 1;
+            cudaMemcpyToSymbol(g_gb_times_on, &on, sizeof(on));
+            const cudaError_t e = gb_dispatch(p.r & 15, grid, nt, smem, p, st, nullptr);
+            cudaDeviceSynchronize();
+            static unsigned long long h[2 * 8192];
+            cudaMemcpyFromSymbol(h, g_gb_times, sizeof(h));
+            const int nb = std::min(8192, (int)(grid.x * grid.y * grid.z));
+            unsigned long long t0 = ~0ull, t1 = 0;
+            for (int i = 0; i < nb; ++i) { t0 = std::min(t0, h[2 * i]); t1 = std::max(t1, h[2 * i + 1]); }
+            fprintf(stderr, "[gb times] ctas=%d span=%.1f us\n", nb, (t1 - t0) * 1e-3);
+            for (int i = 0; i < nb; ++i)
+                fprintf(stderr, "[gb cta] %d strip=%d band=%d start=%.1f end=%.1f\n", i, i % (int)grid.x,
+                        (i / (int)grid.x) % (int)grid.y, (h[2 * i] - t0) * 1e-3, (h[2 * i + 1] - t0) * 1e-3);
+            return e;
+        }
+        return gb_dispatch(p.r & 15, grid, nt, smem, p, st, nullptr);
+    }
     // warp-specialized kernel when the strip has >= 2 column warps (measured: C4 0.624 vs 0.656
     // ms; single-column-warp strips such as C3's are faster on the classic kernel)
     const int ws_mode = use_ws();
@@ -1324,6 +1910,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         if (print_plan())
             fprintf(stderr, "[dtb plan] ws_kernel cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d\n",
                     p.cols, rows_out, p.r, best_w, best_strips, best_tw, occ, (int)grid.y, p.TH);
+        g_last_kernel = "ws_kernel";
         return ws_dispatch(m, sv, grid, nt, smem, p, st, nullptr, v16);
     }
     const int nt = 32 * best_w;
@@ -1346,6 +1933,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     if (print_plan())
         fprintf(stderr, "[dtb plan] slide_kernel V=%d cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d\n",
                 V, p.cols, rows_out, p.r, best_w, nstrips, best_tw, occ, (int)grid.y, p.TH);
+    g_last_kernel = "slide_kernel";
     return V == 16 ? dispatch_rx<16>(m, sv, grid, nt, smem, p, st, nullptr)
                    : dispatch_rx<32>(m, sv, grid, nt, smem, p, st, nullptr);
 }

@@ -1,0 +1,5 @@
+timeout 180 python -m pytest tests/test_gb_gpu.py -x -q > gpurun_out/gb_pytest.log 2>&1; echo pytest_gb=$?
+tail -3 gpurun_out/gb_pytest.log
+for m in 2 0; do DTB_GB=$m timeout 100 python bench.py --config c4 --steps 50 --warmup 5 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('DTB_GB=$m', d['kernel_ms'], d['roofline']['frac'])"; done
+DTB_GB_TIMES=1 timeout 60 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e 2> gpurun_out/gbtimes.log | tail -1 > /dev/null
+grep "gb times" gpurun_out/gbtimes.log | tail -1

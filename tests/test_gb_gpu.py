@@ -1,0 +1,115 @@
+"""Group-bound Sauvola kernel (gb_kernel, dtb_slide.cu) against the CPU oracle, bit-exact.
+
+The kernel decides 4 adjacent pixels at once from bounds on their window sums and re-decides
+uncertain groups per pixel, so the cases below aim at that split: document pages (almost no
+uncertain groups), uniform noise (many), exact ties (flat windows), every r mod 16 (the
+stream-alignment template), image borders, short images (every row clipped), row bands and
+batches.  DTB_GB=1 forces the kernel wherever it is eligible; dtb_last_kernel() pins that it
+ran."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1210_3165_b200 import _lib, engine, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def force_gb(monkeypatch):
+    monkeypatch.setenv("DTB_GB", "1")
+
+
+def _ran_gb():
+    return _lib.lib().dtb_last_kernel() == b"gb_kernel"
+
+
+def _check(img, win, k, r=128.0, expect_gb=True):
+    got, _ = engine.binarize(img, win, "sauvola", k, r, want_tmap=False)
+    if expect_gb:
+        assert _ran_gb(), _lib.lib().dtb_last_kernel()
+    want, _ = oracle.binarize(img, win, "sauvola", k, r, tmap=False, threads=8)
+    got = got.cpu().numpy()
+    if not np.array_equal(got, want):
+        bad = np.argwhere(got != want)
+        raise AssertionError(f"{len(bad)} mismatches, first at {bad[:5].tolist()} "
+                             f"(win={win} k={k} r={r} shape={img.shape})")
+
+
+def test_c4_crop_w127():
+    img = workloads.c4_image(2048)
+    _check(img, 127, 0.34)
+
+
+@pytest.mark.parametrize("rad", range(31, 47))  # every r mod 16
+def test_every_residue(rad):
+    img = workloads.doc_gray(300, 2608, 40 + rad, 900)
+    _check(img, 2 * rad + 1, 0.34)
+
+
+@pytest.mark.parametrize("rad", [1, 2, 3, 5, 8, 15, 17])
+def test_small_windows_forced(rad):
+    img = workloads.doc_gray(257, 2112, rad, 700)
+    _check(img, 2 * rad + 1, 0.5)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_uniform_noise_many_uncertain(seed):
+    rng = np.random.default_rng(100 + seed)
+    img = rng.integers(0, 256, (260, 2304)).astype(np.uint8)
+    win = int(rng.choice([63, 65, 99, 127, 201, 255]))
+    k = float(rng.choice([0.05, 0.34, 0.5, 1.0]))
+    r = float(rng.choice([128.0, 64.0, 255.0, 1.5]))
+    _check(img, win, k, r)
+
+
+def test_flat_windows_exact_ties():
+    # constant 100 and 200 areas: s = 0 -> t = m (1-k) exactly (k = 0.5: t = 100 at m = 200)
+    img = np.full((300, 2208), 200, np.uint8)
+    img[:, 1000:1600] = 100
+    img[120:180, 300:900] = 0
+    img[::7, ::5] = 100
+    for win, k in ((63, 0.5), (127, 0.5), (101, 0.25)):
+        _check(img, win, k)
+
+
+def test_short_and_wide_images():
+    for h in (1, 2, 5, 40):
+        img = workloads.doc_gray(h, 3008, h, 50)
+        _check(img, 127, 0.34)
+
+
+def test_right_edge_partial_strip():
+    for w in (1808, 2128, 4112):
+        img = workloads.doc_gray(150, w, w, 300)
+        _check(img, 95, 0.34)
+
+
+def test_bands_and_batch():
+    torch = engine.torch_mod()
+    img = workloads.c4_image(2048)[:700, :2048]
+    want, _ = oracle.binarize(img, 127, "sauvola", 0.34, tmap=False, threads=8)
+    dev = torch.from_numpy(img).cuda()
+    for y0, y1 in ((0, 1), (13, 400), (699, 700), (300, 700)):
+        a, z = max(y0 - 63, 0), min(y1 + 63, 700)
+        got = engine.binarize_band(dev[a:z], a, 700, y0, y1, 127, "sauvola", 0.34, 128.0)
+        assert _ran_gb()
+        assert np.array_equal(got.cpu().numpy(), want[y0:y1]), (y0, y1)
+    imgs = np.stack([workloads.doc_gray(256, 2048, s, 300) for s in range(3)])
+    got = engine.binarize_batch(torch.from_numpy(imgs).cuda(), 127, "sauvola", 0.34, 128.0)
+    assert _ran_gb()
+    for i in range(3):
+        assert np.array_equal(got[i].cpu().numpy(),
+                              oracle.binarize(imgs[i], 127, "sauvola", 0.34, tmap=False)[0])
+
+
+def test_ineligible_falls_back(monkeypatch):
+    img = workloads.doc_gray(200, 2112, 9, 300)
+    _check(img, 127, 1.5, expect_gb=False)  # k > 1
+    assert not _ran_gb()
+    got, _ = engine.binarize(img, 127, "niblack", -0.2, 128.0, want_tmap=False)
+    assert not _ran_gb()
+    monkeypatch.setenv("DTB_GB", "0")
+    _check(img, 127, 0.34, expect_gb=False)
+    assert not _ran_gb()
