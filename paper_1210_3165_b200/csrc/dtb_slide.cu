@@ -1112,10 +1112,10 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
 //   fp64 replay), out of line.  On document pages this is ~1e-5 of the groups at W=127.
 // =====================================================================================
 #ifndef GB_STAGES
-#define GB_STAGES 5
+#define GB_STAGES 3  // with 128 registers: 4 CTAs per SM (C4: 0.498 vs 0.584 ms at 5 stages, 168 regs, 3 CTAs)
 #endif
 #ifndef DTB_GB_MAXREG
-#define DTB_GB_MAXREG 168
+#define DTB_GB_MAXREG 128
 #endif
 
 #define GB_NC 2048
@@ -1223,10 +1223,14 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
     uint64_t* empty = full + NS;
     uint8_t* ring = reinterpret_cast<uint8_t*>(empty + NS);
     const int ncw = p.ncw, now = p.now, nthr = 32 * (ncw + now);
-    const int t = threadIdx.x;
+    const int bid = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+    // Warp w issues from SM sub-partition w % 4, so fixed role slots put each role on two
+    // sub-partitions only; with role_div > 0, alternate groups of role_div CTAs swap the slots
+    // (column warps on sub-partitions 2, 3) so co-resident CTAs spread both roles.
+    const bool swap = p.role_div > 0 && ((bid / p.role_div) & 1);
+    const int t = swap ? (int)(threadIdx.x ^ 64u) : (int)threadIdx.x;  // ncw = now = 2
     const int lane = t & 31, warp = t >> 5;
     const bool is_col = warp < ncw;
-    const int bid = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
     if (g_gb_times_on && t == 0 && bid < 8192) g_gb_times[2 * bid] = gtimer();
     const uint8_t* in = p.in + (int64_t)blockIdx.z * p.img_stride;
     const int X0 = (int)blockIdx.x * p.TW;
@@ -1386,7 +1390,7 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
             if (lane == 31) { sWS[8 * b + warp] = iS; sWQ[8 * b + warp] = iQ; }
             nbar_sync(BAR_COLS, 32 * ncw);
             uint32_t bS = iS - TS, bQ = iQ - TQ;
-            for (int w = 0; w < warp; ++w) { bS += sWS[8 * b + w]; bQ += sWQ[8 * b + w]; }
+            if (warp == 1) { bS += sWS[8 * b]; bQ += sWQ[8 * b]; }  // ncw = 2
             // wait until the output warps have consumed row k-2 from this prefix buffer
             nbar_sync(BAR_FREE0 + b, nthr);
             uint32_t* sPS = sm + (2 * b) * 4 * PW + 4 * t;
@@ -1837,8 +1841,11 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         best_tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
         best_w = GB_NC / 1024;
         p.ncw = best_w;
-        p.now = (best_tw + 1023) / 1024;
-        p.role_div = 0;
+        p.now = 2;  // (the role swap below pairs 2 column with 2 output warps)
+        {
+            const char* se = getenv("DTB_GB_SWAP");
+            p.role_div = (se && atoi(se) > 0) ? atoi(se) : 0;
+        }
         p.NC = GB_NC;
         p.TW = best_tw;
         const int nt = 32 * (p.ncw + p.now);
