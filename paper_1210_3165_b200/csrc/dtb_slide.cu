@@ -1118,6 +1118,13 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
 #define DTB_GB_MAXREG 128
 #endif
 
+// acc - (sum of the four bytes of x): dp4a with unsigned a and signed (-1) b bytes
+__device__ __forceinline__ uint32_t dp4a_sub(uint32_t x, uint32_t acc) {
+    uint32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(0xFFFFFFFFu), "r"(acc));
+    return d;
+}
+
 #define GB_NC 2048
 // words of one residue plane: 2 rows of (T+1) chunks
 __host__ __device__ constexpr int gb_plane_words(int NC) { return 8 * (NC / 32 + 1); }
@@ -1327,6 +1334,14 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
             if (lane == 0) mbar_arrive_cnt(&empty[s], warp == 0 ? 1 + now : 1);
         }
 
+        // quarter sums of the column sums (columns 8h..8h+7), then kept incrementally with dp4a
+        uint32_t qS[4], qQ[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int c = 8 * h;
+            qS[h] = ((cS[c] + cS[c + 1]) + (cS[c + 2] + cS[c + 3])) + ((cS[c + 4] + cS[c + 5]) + (cS[c + 6] + cS[c + 7]));
+            qQ[h] = ((cQ[c] + cQ[c + 1]) + (cQ[c + 2] + cQ[c + 3])) + ((cQ[c + 4] + cQ[c + 5]) + (cQ[c + 6] + cQ[c + 7]));
+        }
         for (int k = it.nwarm; k < it.n; ++k) {
             const int y = it.ya + (k - it.nwarm);
             const int s = k % NS;
@@ -1351,6 +1366,13 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
                     cS[j] = cS[j] + ev - ov;
                     cQ[j] = cQ[j] + ev * ev - ov * ov;
                 }
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    qS[h] = dp4a_sub(o[2 * h + 1], dp4a_sub(o[2 * h], __dp4a(e[2 * h + 1], 0x01010101u,
+                                                          __dp4a(e[2 * h], 0x01010101u, qS[h]))));
+                    qQ[h] += __dp4a(e[2 * h + 1], e[2 * h + 1], __dp4a(e[2 * h], e[2 * h], 0u)) -
+                             __dp4a(o[2 * h + 1], o[2 * h + 1], __dp4a(o[2 * h], o[2 * h], 0u));
+                }
             } else if (ein || oin) {
                 // image top / bottom: one of the two rows is outside the image
                 uint32_t e[8];
@@ -1367,17 +1389,15 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
                     cS[j] += sg * ev;
                     cQ[j] += sg * (ev * ev);
                 }
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    qS[h] += sg * __dp4a(e[2 * h + 1], 0x01010101u, __dp4a(e[2 * h], 0x01010101u, 0u));
+                    qQ[h] += sg * __dp4a(e[2 * h + 1], e[2 * h + 1], __dp4a(e[2 * h], e[2 * h], 0u));
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with item k's rows
-            // quarter sums (tree) -> lane total -> warp scan -> cross-warp totals
-            uint32_t qS[4], qQ[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int c = 8 * h;
-                qS[h] = ((cS[c] + cS[c + 1]) + (cS[c + 2] + cS[c + 3])) + ((cS[c + 4] + cS[c + 5]) + (cS[c + 6] + cS[c + 7]));
-                qQ[h] = ((cQ[c] + cQ[c + 1]) + (cQ[c + 2] + cQ[c + 3])) + ((cQ[c + 4] + cQ[c + 5]) + (cQ[c + 6] + cQ[c + 7]));
-            }
+            // lane total -> warp scan -> cross-warp totals
             const uint32_t TS = (qS[0] + qS[1]) + (qS[2] + qS[3]);
             const uint32_t TQ = (qQ[0] + qQ[1]) + (qQ[2] + qQ[3]);
             uint32_t iS = TS, iQ = TQ;
