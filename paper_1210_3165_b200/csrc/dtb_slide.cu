@@ -663,6 +663,7 @@ __device__ __forceinline__ void nbar_sync(int id, int count) {
 }
 __device__ __forceinline__ void nbar_arrive(int id, int count) {
     switch (id) {
+        case 1: nbar_arrive_c<1>(count); break;
         case 2: nbar_arrive_c<2>(count); break;
         case 3: nbar_arrive_c<3>(count); break;
         case 4: nbar_arrive_c<4>(count); break;
@@ -1350,54 +1351,39 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
             const uint8_t* stage = ring + (size_t)s * 3 * NC;
             const bool first = (k == it.nwarm);
             const bool ein = !first && y + p.r < p.H, oin = !first && y - p.r - 1 >= 0;
-            if (ein && oin) {
-                uint32_t e[8], o[8];
+            // entering / leaving row bytes of this lane's 32 columns (zero when outside the image)
+            uint32_t e[8], o[8];
+            {
                 const uint4* E = reinterpret_cast<const uint4*>(stage + 32 * t);
                 const uint4* O = reinterpret_cast<const uint4*>(stage + NC + 32 * t);
+                if (ein && oin) {
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const uint4 a = E[q], bb = O[q];
-                    e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
-                    o[4 * q] = bb.x; o[4 * q + 1] = bb.y; o[4 * q + 2] = bb.z; o[4 * q + 3] = bb.w;
-                }
+                    for (int q = 0; q < 2; ++q) {
+                        const uint4 a = E[q], bb = O[q];
+                        e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
+                        o[4 * q] = bb.x; o[4 * q + 1] = bb.y; o[4 * q + 2] = bb.z; o[4 * q + 3] = bb.w;
+                    }
+                } else {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
-                    cS[j] = cS[j] + ev - ov;
-                    cQ[j] = cQ[j] + ev * ev - ov * ov;
-                }
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    qS[h] = dp4a_sub(o[2 * h + 1], dp4a_sub(o[2 * h], __dp4a(e[2 * h + 1], 0x01010101u,
-                                                          __dp4a(e[2 * h], 0x01010101u, qS[h]))));
-                    qQ[h] += __dp4a(e[2 * h + 1], e[2 * h + 1], __dp4a(e[2 * h], e[2 * h], 0u)) -
-                             __dp4a(o[2 * h + 1], o[2 * h + 1], __dp4a(o[2 * h], o[2 * h], 0u));
-                }
-            } else if (ein || oin) {
-                // image top / bottom: one of the two rows is outside the image
-                uint32_t e[8];
-                const uint4* E = reinterpret_cast<const uint4*>(stage + (ein ? 0 : NC) + 32 * t);
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const uint4 a = E[q];
-                    e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
-                }
-                const uint32_t sg = ein ? 1u : 0xFFFFFFFFu;  // +1 entering, -1 leaving
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t ev = byte_at(e, j);
-                    cS[j] += sg * ev;
-                    cQ[j] += sg * (ev * ev);
-                }
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    qS[h] += sg * __dp4a(e[2 * h + 1], 0x01010101u, __dp4a(e[2 * h], 0x01010101u, 0u));
-                    qQ[h] += sg * __dp4a(e[2 * h + 1], e[2 * h + 1], __dp4a(e[2 * h], e[2 * h], 0u));
+                    for (int q = 0; q < 2; ++q) {
+                        const uint4 a = ein ? E[q] : make_uint4(0, 0, 0, 0);
+                        const uint4 bb = oin ? O[q] : make_uint4(0, 0, 0, 0);
+                        e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
+                        o[4 * q] = bb.x; o[4 * q + 1] = bb.y; o[4 * q + 2] = bb.z; o[4 * q + 3] = bb.w;
+                    }
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with item k's rows
-            // lane total -> warp scan -> cross-warp totals
+            // quarter totals (dp4a) -> lane total -> warp scan; the scan's shuffle latency and
+            // the column-warp hand-off overlap the vertical update below
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                qS[h] = dp4a_sub(o[2 * h + 1], dp4a_sub(o[2 * h], __dp4a(e[2 * h + 1], 0x01010101u,
+                                                      __dp4a(e[2 * h], 0x01010101u, qS[h]))));
+                qQ[h] += __dp4a(e[2 * h + 1], e[2 * h + 1], __dp4a(e[2 * h], e[2 * h], 0u)) -
+                         __dp4a(o[2 * h + 1], o[2 * h + 1], __dp4a(o[2 * h], o[2 * h], 0u));
+            }
             const uint32_t TS = (qS[0] + qS[1]) + (qS[2] + qS[3]);
             const uint32_t TQ = (qQ[0] + qQ[1]) + (qQ[2] + qQ[3]);
             uint32_t iS = TS, iQ = TQ;
@@ -1407,10 +1393,22 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
                 const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
                 if (lane >= off) { iS += vs; iQ += vq; }
             }
-            if (lane == 31) { sWS[8 * b + warp] = iS; sWQ[8 * b + warp] = iQ; }
-            nbar_sync(BAR_COLS, 32 * ncw);
+            // column warp 0 hands its total to warp 1 (ncw = 2): arrive now, warp 1 syncs later
+            if (warp == 0) {
+                if (lane == 31) { sWS[8 * b] = iS; sWQ[8 * b] = iQ; }
+                nbar_arrive(BAR_COLS, 32 * ncw);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
+                cS[j] = cS[j] + ev - ov;
+                cQ[j] = cQ[j] + ev * ev - ov * ov;
+            }
             uint32_t bS = iS - TS, bQ = iQ - TQ;
-            if (warp == 1) { bS += sWS[8 * b]; bQ += sWQ[8 * b]; }  // ncw = 2
+            if (warp == 1) {
+                nbar_sync(BAR_COLS, 32 * ncw);
+                bS += sWS[8 * b]; bQ += sWQ[8 * b];
+            }
             // wait until the output warps have consumed row k-2 from this prefix buffer
             nbar_sync(BAR_FREE0 + b, nthr);
             uint32_t* sPS = sm + (2 * b) * 4 * PW + 4 * t;
