@@ -1173,29 +1173,66 @@ __device__ __forceinline__ uint32_t gb_ceil2(float x) {
     return bits * 0x10001u - 0x4B000000u * 0x10001u;
 }
 
-// Uncertain group of 4 pixels (gb_kernel), out of line: exact S, Q per pixel from the
-// residue-decimated prefix, certified fp32 decision, reference fp64 replay when within tol.
+// Uncertain group of 4 pixels x0..x0+3 (gb_kernel), out of line.  First a tighter lower
+// bound: the window contains the group's intersection window I, and a subset's squared
+// deviations about its own mean bound the window's from below, so var >= (n_I/n) var_I
+// (var_I = Q_I/n_I - m_I^2, evaluated lowered) and t >= m_lo ((1-k) + (k/R) s_lo).  Pixels the
+// refined bounds still leave open get exact S, Q from the residue-decimated prefix, the
+// certified fp32 decision and, within tol, the reference fp64 replay.  All four bytes are
+// rewritten after the caller's vector stores (program order).
 __device__ __noinline__ void gb_fix_group(const uint32_t* sPS, const uint32_t* sPQ, int PW, int T1,
                                           int a_word, int b_word, const uint8_t* f4, uint8_t* orow,
                                           int x0, int cols, int ny, int r, float cA, float cC,
                                           float ca, float cc, float tol, double kk, double rr) {
+    const float kUp = 1.0f + 7.62939453125e-6f, kDn = 1.0f - 7.62939453125e-6f;  // 1 +- 2^-17
+    int nmin = 1 << 30, nmax = 0;
+    for (int i = 0; i < 4; ++i) {
+        const int x = x0 + i;
+        const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
+        nmin = min(nmin, nx); nmax = max(nmax, nx);
+    }
+    nmin = max(nmin, 1);
+    const float rlo = rcp_ftz((float)(ny * nmin)) * kUp, rhi = rcp_ftz((float)(ny * nmax)) * kDn;
+    const uint32_t pa0 = gb_word(sPS, PW, T1, a_word), pa3 = gb_word(sPS, PW, T1, a_word + 3);
+    const uint32_t pb0 = gb_word(sPS, PW, T1, b_word), pb3 = gb_word(sPS, PW, T1, b_word + 3);
+    const uint32_t qa0 = gb_word(sPQ, PW, T1, a_word), qa3 = gb_word(sPQ, PW, T1, a_word + 3);
+    const uint32_t qb0 = gb_word(sPQ, PW, T1, b_word), qb3 = gb_word(sPQ, PW, T1, b_word + 3);
+    const float fSI = (float)(pb0 - pa3);
+    const float mhi = (float)(pb3 - pa0) * rlo, mlo = fSI * rhi;
+    const float v = __fmaf_rn((float)(qb3 - qa0), rlo, -(mlo * mlo));
+    const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sqrt_ftz(fmaxf(v, 0.f)), cc, ca), tol), 4096.f);
+    const int nxI = min(x0 + r, cols - 1) - max(x0 + 3 - r, 0) + 1;
+    float sl = 0.f;
+    if (nxI >= 1) {
+        const float nI = (float)(ny * nxI), rnI = rcp_ftz(nI);
+        const float mI = fSI * (rnI * kUp);
+        const float vI = __fmaf_rn((float)(qb0 - qa3), rnI * kDn, -(mI * mI));
+        sl = sqrt_ftz(fmaxf(vI, 0.f) * (nI * rhi));
+    }
+    const float tlo = __fmaf_rn(mlo, __fmaf_rn(sl, cc * kDn, ca), -tol);
     for (int i = 0; i < 4; ++i) {
         const int x = x0 + i;
         if (x >= cols) break;
-        const uint32_t S = gb_word(sPS, PW, T1, b_word + i) - gb_word(sPS, PW, T1, a_word + i);
-        const uint32_t Q = gb_word(sPQ, PW, T1, b_word + i) - gb_word(sPQ, PW, T1, a_word + i);
         const uint32_t f = f4[i];
-        const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
-        const uint32_t n = (uint32_t)(ny * nx);
-        const float d = fast_diff<DTB_METHOD_SAUVOLA, true>(S, Q, f, n, cA, cC, ca, cc);
         uint32_t white;
-        if (fabsf(d) >= tol) {
-            white = d < 0.f ? 0u : 0xFFu;
+        if ((float)f < tlo) {
+            white = 0u;
+        } else if ((float)f >= thi) {
+            white = 0xFFu;
         } else {
-            white = exact_white(S, Q, (double)n, f, DTB_METHOD_SAUVOLA, kk, rr);
-            if (unsigned long long* audit = g_fp32_audit) {
-                atomicAdd(&audit[0], 1ull);
-                if (white != (d < 0.f ? 0u : 0xFFu)) atomicAdd(&audit[1], 1ull);
+            const uint32_t S = gb_word(sPS, PW, T1, b_word + i) - gb_word(sPS, PW, T1, a_word + i);
+            const uint32_t Q = gb_word(sPQ, PW, T1, b_word + i) - gb_word(sPQ, PW, T1, a_word + i);
+            const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
+            const uint32_t n = (uint32_t)(ny * nx);
+            const float d = fast_diff<DTB_METHOD_SAUVOLA, true>(S, Q, f, n, cA, cC, ca, cc);
+            if (fabsf(d) >= tol) {
+                white = d < 0.f ? 0u : 0xFFu;
+            } else {
+                white = exact_white(S, Q, (double)n, f, DTB_METHOD_SAUVOLA, kk, rr);
+                if (unsigned long long* audit = g_fp32_audit) {
+                    atomicAdd(&audit[0], 1ull);
+                    if (white != (d < 0.f ? 0u : 0xFFu)) atomicAdd(&audit[1], 1ull);
+                }
             }
         }
         orow[x] = (uint8_t)white;
@@ -1503,17 +1540,21 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
                 gb_stream<D_B3>(sPS + R_B3 * PW, to + qB3, T1, SB3);
                 gb_stream<D_A0>(sPQ + R_A0 * PW, to, T1, QA0);
                 gb_stream<D_B3>(sPQ + R_B3 * PW, to + qB3, T1, QB3);
-                // 1/n for the row (interior lanes: n = ny * W for every pixel), with the slack
+                // 1/n for the row (interior lanes: n = ny * W for every pixel), with the slack;
+                // the intersection window I has n_I = ny (2r-2) pixels
                 const float rnr = rcp_ftz((float)ny * W);  // rel. error << the 2^-17 slack
                 const float rloR = rnr * kUp, rhiR = rnr * kDn;
                 uint32_t ow[8];
                 uint32_t um = 0;  // groups with an uncertain pixel
+                // rlo / rhi: 1/n_lo, 1/n_hi with the slack
                 auto group = [&](int g, float rlo, float rhi) {
                     const uint32_t SU = SB3[g] - SA0[g];
                     const uint32_t SI = SB0[g] - SA3[g];
                     const uint32_t QU = QB3[g] - QA0[g];
+                    const float fSI = (float)SI;
                     const float mhi = (float)SU * rlo;
-                    const float mlo = (float)SI * rhi;
+                    const float mlo = fSI * rhi;
+                    // upper: var <= Q_U/n_lo - m_lo^2 (raised)
                     const float v = __fmaf_rn((float)QU, rlo, -(mlo * mlo));
                     const float sd = sqrt_ftz(fmaxf(v, 0.f));
                     const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sd, cK, a1), dAbs), 4096.f);
@@ -1814,6 +1855,12 @@ static cudaError_t gb_dispatch(int r16, dim3 grid, int nt, size_t smem, const Sl
 #ifndef DTB_GB_MIN_COLS
 #define DTB_GB_MIN_COLS 1536
 #endif
+// Auto mode also wants a large page: on 4096^2 pages with sigma-12 noise (C5) many groups need
+// the out-of-line re-decision and the one-wave plan has ~20-row bands under 2r+1 warm-up rows,
+// which measured 1.1-1.3x slower than ws_kernel at W 67..179 (profiles/r01d_config_table.json).
+#ifndef DTB_GB_MIN_PIXELS
+#define DTB_GB_MIN_PIXELS (1ll << 26)
+#endif
 static int gb_mode() {  // read per launch (tests switch it)
     const char* e = getenv("DTB_GB");
     return e ? atoi(e) : 2;
@@ -1853,7 +1900,8 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     const int gb_tw = 32 * ((GB_NC - 2 * p.rx - alpha) / 32);
     if (V == 32 && !p.nseg && p.method == DTB_METHOD_SAUVOLA && p.k > 0.0 && p.k <= 1.0 &&
         p.rx == p.r && gb_tw >= 32 &&
-        (gbm == 1 || (gbm == 2 && p.r >= DTB_GB_MIN_R && p.cols >= DTB_GB_MIN_COLS))) {
+        (gbm == 1 || (gbm == 2 && p.r >= DTB_GB_MIN_R && p.cols >= DTB_GB_MIN_COLS &&
+                      (long long)p.cols * (p.out_end - p.out_begin) * n_images >= DTB_GB_MIN_PIXELS))) {
         const int ns = (p.cols + gb_tw - 1) / gb_tw;
         best_strips = ns;
         best_tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
@@ -1872,12 +1920,31 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         const cudaError_t qe = gb_dispatch(p.r & 15, dim3(), nt, smem, p, st, &occ);
         if (qe != cudaSuccess) return qe;
         const int slots = num_sms * occ;
-        // two waves of bands: content-dependent band cost (uncertain groups cluster in dark
-        // page regions) leaves a one-wave launch waiting on its slowest bands (C4: 0.538 vs 0.583 ms)
-        const char* bse = getenv("DTB_BAND_SCALE");
-        const double bscale = bse ? band_scale() : 2.0;
-        int nbands = std::max(1, (int)(bscale * slots / std::max(1, best_strips * n_images)));
-        nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
+        // Band count from a cost model, in main-row units per CTA slot:
+        //   waves * (TH + 0.25 (2r+1))  +  0.3 TH
+        // (a warm-up row -- column sums only -- costs ~1/4 of a main row; the last term stands
+        // for the content-dependent spread of band cost: uncertain groups cluster in dark page
+        // regions, and a one-wave launch waits on its slowest bands).  C4: 2 waves of 125-row
+        // bands (0.498 ms vs 0.518 at one wave); 4096^2 pages: one wave (bands of 2r+1 rows of
+        // warm-up over ~20 output rows otherwise dominate).
+        int nbands = 1;
+        {
+            const char* bse = getenv("DTB_BAND_SCALE");
+            const int units = std::max(1, best_strips * n_images);
+            if (bse) {
+                nbands = std::max(1, (int)(band_scale() * slots / units));
+            } else {
+                double best_cost = 1e300;
+                const int nb_max = std::max(1, std::min((rows_out + 7) / 8, 4 * slots / units + 1));
+                for (int nb = 1; nb <= nb_max; ++nb) {
+                    const int th = (rows_out + nb - 1) / nb;
+                    const int waves = (units * nb + slots - 1) / slots;
+                    const double cost = waves * (th + 0.25 * (2 * p.r + 1)) + 0.3 * th;
+                    if (cost < best_cost) { best_cost = cost; nbands = nb; }
+                }
+            }
+            nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
+        }
         p.TH = (rows_out + nbands - 1) / nbands;
         dim3 grid(best_strips, (rows_out + p.TH - 1) / p.TH, n_images);
         if (print_plan())
