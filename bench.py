@@ -317,6 +317,8 @@ def run_ours(a):
     clocks = sampler.stop() if sampler else None
     ms = t0.elapsed_time(t1) / a.steps
     kms = statistics.fmean(s.elapsed_time(e) for s, e in kev)
+    from paper_1210_3165_b200 import _lib as _dl
+    kernel_name = _dl.lib().dtb_last_kernel().decode() or None  # the timed launches' kernel
     if world > 1:
         t = torch.tensor([ms, kms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -365,7 +367,7 @@ def run_ours(a):
                        "l2": (f"{nrot} rotating input/output buffer sets, "
                               f"{nrot * per_step_bytes / 2**20:.0f} MiB per rank >= 2x L2 "
                               f"({l2 / 2**20:.0f} MiB)")},
-            "kernel_ms": round(kms, 5),
+            "kernel_ms": round(kms, 5), "kernel": kernel_name,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",

@@ -1289,9 +1289,13 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
     const int c_hi16 = c_lo + ((max(c_hi - c_lo, 0)) & ~15);
     const int f_hi = min(X0 + p.TW, p.cols);
     const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
+    // Items: warm-up items first, each carrying up to three warm-up rows (in the entering,
+    // leaving and centre slots -- a warm-up row needs only its bytes), then one item per output
+    // row.  Packing triples the warm-up rows in flight on the 3-stage ring.
     Items it;
     it.g0 = max(ya - p.r, 0);
-    it.nwarm = min(ya + p.r, p.H - 1) - it.g0 + 1;
+    const int nwr = min(ya + p.r, p.H - 1) - it.g0 + 1;  // warm-up rows
+    it.nwarm = (nwr + 2) / 3;                             // warm-up items
     it.ya = ya;
     it.n = it.nwarm + (yb - ya);
 
@@ -1318,7 +1322,16 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
         uint8_t* F = O + NC;
         int ge, go = -1, gf = -1;
         if (k < it.nwarm) {
-            ge = it.g0 + k;
+            // warm-up rows g0+3k .. g0+3k+2 into the E, O, F slots (full strip width each)
+            const uint32_t rowb = (uint32_t)(c_hi16 - c_lo);
+            const int g = it.g0 + 3 * k, cnt = min(3, it.g0 + nwr - g);
+            mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
+            for (int i = 0; i < cnt; ++i) {
+                uint8_t* D = E + i * NC;
+                if (rowb) bulk_g2s(D + (c_lo - xc0), in0 + (int64_t)(g + i) * p.pitch + c_lo, rowb, &full[s], pol_keep);
+                for (int c = c_hi16; c < c_hi; ++c) D[c - xc0] = in0[(int64_t)(g + i) * p.pitch + c];
+            }
+            return;
         } else {
             const int y = it.ya + (k - it.nwarm);
             gf = y;
@@ -1355,18 +1368,21 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
         for (int k = 0; k < it.nwarm; ++k) {
             const int s = k % NS;
             mbar_wait(&full[s], (k / NS) & 1);
-            const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * NC + 32 * t);
-            uint32_t w[8];
+            const int cnt = min(3, nwr - 3 * k);
+            for (int i = 0; i < cnt; ++i) {
+                const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * NC + i * NC + 32 * t);
+                uint32_t w[8];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const uint4 a = E[q];
-                w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
-            }
+                for (int q = 0; q < 2; ++q) {
+                    const uint4 a = E[q];
+                    w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+                }
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t v = byte_at(w, j);
-                cS[j] += v;
-                cQ[j] += v * v;
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t v = byte_at(w, j);
+                    cS[j] += v;
+                    cQ[j] += v * v;
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive_cnt(&empty[s], warp == 0 ? 1 + now : 1);
