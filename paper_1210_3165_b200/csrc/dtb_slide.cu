@@ -1249,7 +1249,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // R16 = r & 15 (fixes every stream's alignment); interior rows/lanes use n = (2r+1)^2.
-template <int R16>
+// SEG: segmented input (dtb_binarize_segments, e.g. halo rows read in place from a
+// neighbour GPU's band over NVLink); a compile-time variant like ws_kernel's.
+template <int R16, bool SEG>
 __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
     constexpr int NS = GB_STAGES;
     constexpr int ALPHA = (16 - R16) & 15;
@@ -1328,8 +1330,8 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
             mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
             for (int i = 0; i < cnt; ++i) {
                 uint8_t* D = E + i * NC;
-                if (rowb) bulk_g2s(D + (c_lo - xc0), in0 + (int64_t)(g + i) * p.pitch + c_lo, rowb, &full[s], pol_keep);
-                for (int c = c_hi16; c < c_hi; ++c) D[c - xc0] = in0[(int64_t)(g + i) * p.pitch + c];
+                if (rowb) bulk_g2s(D + (c_lo - xc0), row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
+                for (int c = c_hi16; c < c_hi; ++c) D[c - xc0] = row_at<SEG>(p, in0, g + i)[c];
             }
             return;
         } else {
@@ -1345,15 +1347,15 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
         if (go >= 0) bytes += rowb;
         if (gf >= 0) bytes += fb;
         mbar_expect_tx(&full[s], bytes);
-        if (ge >= 0 && rowb) bulk_g2s(E + (c_lo - xc0), in0 + (int64_t)ge * p.pitch + c_lo, rowb, &full[s], pol_keep);
-        if (go >= 0 && rowb) bulk_g2s(O + (c_lo - xc0), in0 + (int64_t)go * p.pitch + c_lo, rowb, &full[s], pol_drop);
-        if (gf >= 0 && fb) bulk_g2s(F, in0 + (int64_t)gf * p.pitch + X0, fb, &full[s], pol_keep);
+        if (ge >= 0 && rowb) bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
+        if (go >= 0 && rowb) bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+        if (gf >= 0 && fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
         for (int c = c_hi16; c < c_hi; ++c) {
-            if (ge >= 0) E[c - xc0] = in0[(int64_t)ge * p.pitch + c];
-            if (go >= 0) O[c - xc0] = in0[(int64_t)go * p.pitch + c];
+            if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
+            if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
         }
         for (int c = f_hi16; c < f_hi; ++c)
-            if (gf >= 0) F[c - X0] = in0[(int64_t)gf * p.pitch + c];
+            if (gf >= 0) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
     };
 
     // The producer is lane 0 of the first OUTPUT warp: it refills a ring slot once all four
@@ -1823,11 +1825,11 @@ static double band_scale() {
 }
 
 // ---- group-bound launcher (gb_kernel)
-template <int R16>
+template <int R16, bool SEG>
 static cudaError_t gb_run(dim3 grid, int nt, size_t smem, const SlideParams& p, cudaStream_t st,
                           int* occ) {
     static size_t granted = 48 * 1024;
-    auto kern = gb_kernel<R16>;
+    auto kern = gb_kernel<R16, SEG>;
     if (smem > granted) {
         const cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1854,7 +1856,8 @@ static cudaError_t gb_run(dim3 grid, int nt, size_t smem, const SlideParams& p, 
 static cudaError_t gb_dispatch(int r16, dim3 grid, int nt, size_t smem, const SlideParams& p,
                                cudaStream_t st, int* occ) {
     switch (r16) {
-#define DTB_GB_CASE(R) case R: return gb_run<R>(grid, nt, smem, p, st, occ);
+#define DTB_GB_CASE(R) case R: return p.nseg ? gb_run<R, true>(grid, nt, smem, p, st, occ) \
+                                              : gb_run<R, false>(grid, nt, smem, p, st, occ);
         DTB_GB_CASE(0) DTB_GB_CASE(1) DTB_GB_CASE(2) DTB_GB_CASE(3)
         DTB_GB_CASE(4) DTB_GB_CASE(5) DTB_GB_CASE(6) DTB_GB_CASE(7)
         DTB_GB_CASE(8) DTB_GB_CASE(9) DTB_GB_CASE(10) DTB_GB_CASE(11)
@@ -1914,7 +1917,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // group-bound kernel: Sauvola with 0 < k <= 1, strips of 2 column warps (see gb_kernel)
     const int gbm = gb_mode();
     const int gb_tw = 32 * ((GB_NC - 2 * p.rx - alpha) / 32);
-    if (V == 32 && !p.nseg && p.method == DTB_METHOD_SAUVOLA && p.k > 0.0 && p.k <= 1.0 &&
+    if (V == 32 && p.method == DTB_METHOD_SAUVOLA && p.k > 0.0 && p.k <= 1.0 &&
         p.rx == p.r && gb_tw >= 32 &&
         (gbm == 1 || (gbm == 2 && p.r >= DTB_GB_MIN_R && p.cols >= DTB_GB_MIN_COLS &&
                       (long long)p.cols * (p.out_end - p.out_begin) * n_images >= DTB_GB_MIN_PIXELS))) {

@@ -113,3 +113,18 @@ def test_ineligible_falls_back(monkeypatch):
     monkeypatch.setenv("DTB_GB", "0")
     _check(img, 127, 0.34, expect_gb=False)
     assert not _ran_gb()
+
+
+def test_segmented_input_matches_page():
+    # dtb_binarize_segments (halo rows in other buffers, e.g. a neighbour GPU's band over
+    # NVLink) on the group-bound kernel's SEG variant
+    torch = engine.torch_mod()
+    img = workloads.c4_image(2048)[:900, :2048]
+    want, _ = oracle.binarize(img, 127, "sauvola", 0.34, tmap=False, threads=8)
+    dev = torch.from_numpy(img).cuda()
+    top, mid, bot = dev[:200].clone(), dev[200:700].clone(), dev[700:].clone()
+    segs = [(t.data_ptr(), t.stride(0), t.shape[0], t.shape[1]) for t in (top, mid, bot)]
+    for y0, y1 in ((263, 637), (0, 900), (640, 900)):
+        out = engine.binarize_segments(segs, 0, 900, y0, y1, 127, "sauvola", 0.34, 128.0)
+        assert _ran_gb()
+        assert np.array_equal(out.cpu().numpy(), want[y0:y1]), (y0, y1)
