@@ -1917,8 +1917,10 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // group-bound kernel: Sauvola with 0 < k <= 1, strips of 2 column warps (see gb_kernel)
     const int gbm = gb_mode();
     const int gb_tw = 32 * ((GB_NC - 2 * p.rx - alpha) / 32);
+    // r <= 127: the union window's Q_U (2r+4 columns) stays below 2^32 (65025 * 258 * 255);
+    // slide_ok alone admits W = 257, whose union sums could wrap
     if (V == 32 && p.method == DTB_METHOD_SAUVOLA && p.k > 0.0 && p.k <= 1.0 &&
-        p.rx == p.r && gb_tw >= 32 &&
+        p.rx == p.r && p.r <= 127 && gb_tw >= 32 &&
         (gbm == 1 || (gbm == 2 && p.r >= DTB_GB_MIN_R && p.cols >= DTB_GB_MIN_COLS &&
                       (long long)p.cols * (p.out_end - p.out_begin) * n_images >= DTB_GB_MIN_PIXELS))) {
         const int ns = (p.cols + gb_tw - 1) / gb_tw;

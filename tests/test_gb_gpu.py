@@ -128,3 +128,13 @@ def test_segmented_input_matches_page():
         out = engine.binarize_segments(segs, 0, 900, y0, y1, 127, "sauvola", 0.34, 128.0)
         assert _ran_gb()
         assert np.array_equal(out.cpu().numpy(), want[y0:y1]), (y0, y1)
+
+
+def test_w257_stays_off_gb():
+    # W = 257 passes the sliding kernels' 2^32 bound but the union window (2r+4 columns)
+    # would not: the group-bound kernel must not run, and a saturated page stays exact
+    img = np.full((600, 2112), 255, np.uint8)
+    img[::3, ::7] = 254
+    _check(img, 257, 0.34, expect_gb=False)
+    assert not _ran_gb()
+    _check(img, 255, 0.34)  # W = 255 is the largest window the kernel takes
