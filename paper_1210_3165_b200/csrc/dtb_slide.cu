@@ -1732,11 +1732,12 @@ static cudaError_t dispatch_rx(int m, bool sv, dim3 grid, int nt, size_t smem,
     return cudaErrorInvalidValue;
 }
 
+// DTB_SLIDE_V=16 / 32 forces the columns per thread of the sliding kernels; unset = auto
 static int slide_v() {
-    static int v = 0;
-    if (v == 0) {
+    static int v = -1;
+    if (v < 0) {
         const char* env = getenv("DTB_SLIDE_V");
-        v = (env && atoi(env) == 16) ? 16 : 32;
+        v = env ? (atoi(env) == 16 ? 16 : 32) : 0;
     }
     return v;
 }
@@ -1895,24 +1896,28 @@ cudaError_t set_fp32_audit(unsigned long long* counters) {
 
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
     slide_constants(p);
-    const int V = p.nseg ? 32 : slide_v();  // segmented variants exist for V = 32 only
+    const int vset = slide_v();
+    int V = p.nseg ? 32 : (vset ? vset : 32);  // segmented variants exist for V = 32 only
     const int rows_out = p.out_end - p.out_begin;
     const int alpha = (16 - (p.rx & 15)) & 15;
     // strip plan: w warps -> NC = 32 V w columns; pick the w (1..8) with the least total column
     // work (strips x NC) for this image width, balancing the strips' output widths.
-    int best_w = 0, best_strips = 0, best_tw = 0;
-    long best_work = 0;
-    for (int w = 1; w <= 8; ++w) {
-        const int nc = 32 * V * w;
-        const int twmax = 32 * ((nc - 2 * p.rx - alpha) / 32);
-        if (twmax < 32) continue;
-        const int ns = (p.cols + twmax - 1) / twmax;
-        const int tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
-        const long work = (long)ns * nc;
-        if (best_w == 0 || work < best_work) {
-            best_w = w; best_strips = ns; best_tw = tw; best_work = work;
+    struct Plan { int w, strips, tw; long work; };
+    auto plan_for = [&](int Vx) {
+        Plan b{0, 0, 0, 0};
+        for (int w = 1; w <= 8; ++w) {
+            const int nc = 32 * Vx * w;
+            const int twmax = 32 * ((nc - 2 * p.rx - alpha) / 32);
+            if (twmax < 32) continue;
+            const int ns = (p.cols + twmax - 1) / twmax;
+            const int tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
+            const long work = (long)ns * nc;
+            if (b.w == 0 || work < b.work) b = Plan{w, ns, tw, work};
         }
-    }
+        return b;
+    };
+    Plan pl = plan_for(V);
+    int best_w = pl.w, best_strips = pl.strips, best_tw = pl.tw;
     if (best_w == 0) return cudaErrorInvalidValue;  // window too wide for 8 warps (caller checks)
     // group-bound kernel: Sauvola with 0 < k <= 1, strips of 2 column warps (see gb_kernel)
     const int gbm = gb_mode();
@@ -1990,6 +1995,17 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
             return e;
         }
         return gb_dispatch(p.r & 15, grid, nt, smem, p, st, nullptr);
+    }
+    // Auto V: 16 columns per thread give strips in 512-column steps (and 128-register warps);
+    // take them when that cuts the staged column work by >= 15% (C2 pages 2480 wide: one strip
+    // of 2560 instead of three of 1024 -- W15 0.119 -> 0.058 ms; C5 W195+: 6144 -> 5120 columns,
+    // 5-7% faster).  Smaller savings measured no gain or a loss (C5 W19..W179).
+    if (!vset && !p.nseg && V == 32) {
+        const Plan p16 = plan_for(16);
+        if (p16.w > 0 && p16.work * 100 < pl.work * 85) {
+            V = 16;
+            best_w = p16.w; best_strips = p16.strips; best_tw = p16.tw;
+        }
     }
     // warp-specialized kernel when the strip has >= 2 column warps (measured: C4 0.624 vs 0.656
     // ms; single-column-warp strips such as C3's are faster on the classic kernel)
