@@ -138,3 +138,24 @@ def test_w257_stays_off_gb():
     _check(img, 257, 0.34, expect_gb=False)
     assert not _ran_gb()
     _check(img, 255, 0.34)  # W = 255 is the largest window the kernel takes
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_pages_and_params(seed):
+    rng = np.random.default_rng(2000 + seed)
+    for _ in range(4):
+        h = int(rng.integers(1, 500))
+        w = 16 * int(rng.integers(100, 270))  # 1600..4300 columns, 16-byte rows
+        kind = int(rng.integers(0, 3))
+        if kind == 0:
+            img = workloads.doc_gray(h, w, int(rng.integers(0, 1 << 30)), max(1, h * w // 3000))
+        elif kind == 1:
+            img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+        else:  # flat levels + small noise: many near-ties
+            base = rng.integers(0, 256, (1, w // 64 + 1)).repeat(64, 1)[:, :w]
+            img = np.clip(base + rng.integers(-3, 4, (h, w)), 0, 255).astype(np.uint8)
+        win = int(2 * rng.integers(1, 128) + 1)
+        k = float(rng.choice([0.01, 0.2, 0.34, 0.5, 0.77, 1.0]))
+        r = float(rng.choice([1.0, 16.0, 128.0, 255.0, 300.0]))
+        expect = (2 * (win // 2) + 16 <= 2048) and h > 0
+        _check(img, win, k, r, expect_gb=expect and (win // 2) <= 127)
