@@ -1126,7 +1126,10 @@ __device__ __forceinline__ uint32_t dp4a_sub(uint32_t x, uint32_t acc) {
     return d;
 }
 
-#define GB_NC 2048
+#ifndef GB_NCW
+#define GB_NCW 2  // column warps (= output warps) per CTA; NC = 1024 * GB_NCW strip columns
+#endif
+#define GB_NC (1024 * GB_NCW)
 // words of one residue plane: 2 rows of (T+1) chunks
 __host__ __device__ constexpr int gb_plane_words(int NC) { return 8 * (NC / 32 + 1); }
 
@@ -1261,7 +1264,7 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
     constexpr int D_B0 = (EB >> 2) & 7, D_B3 = ((EB + 3) >> 2) & 7;
     constexpr int R_A0 = ALPHA & 3, R_A3 = (ALPHA + 3) & 3, R_B0 = EB & 3, R_B3 = (EB + 3) & 3;
     extern __shared__ __align__(128) uint32_t sm[];
-    constexpr int NC = GB_NC;  // 2 column warps (the host launches gb_kernel only with ncw = 2)
+    constexpr int NC = GB_NC;  // GB_NCW column warps (the host launches with ncw = now = GB_NCW)
     constexpr int PW = gb_plane_words(NC);
     constexpr int T = NC / 32, T1 = T + 1;
     uint32_t* sWS = sm + 16 * PW;  // [2][8] per-column-warp totals, double buffered
@@ -1275,7 +1278,7 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
     // sub-partitions only; with role_div > 0, alternate groups of role_div CTAs swap the slots
     // (column warps on sub-partitions 2, 3) so co-resident CTAs spread both roles.
     const bool swap = p.role_div > 0 && ((bid / p.role_div) & 1);
-    const int t = swap ? (int)(threadIdx.x ^ 64u) : (int)threadIdx.x;  // ncw = now = 2
+    const int t = swap ? (int)(threadIdx.x ^ (32u * GB_NCW)) : (int)threadIdx.x;  // ncw = now
     const int lane = t & 31, warp = t >> 5;
     const bool is_col = warp < ncw;
     if (g_gb_times_on && t == 0 && bid < 8192) g_gb_times[2 * bid] = gtimer();
@@ -1448,11 +1451,13 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
                 const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
                 if (lane >= off) { iS += vs; iQ += vq; }
             }
-            // column warp 0 hands its total to warp 1 (ncw = 2): arrive now, warp 1 syncs later
-            if (warp == 0) {
+            // column warp 0 hands its total to warp 1 (ncw = 2): arrive now, warp 1 syncs later;
+            // with more column warps every warp publishes and all sync after the update
+            if (GB_NCW == 2 && warp == 0) {
                 if (lane == 31) { sWS[8 * b] = iS; sWQ[8 * b] = iQ; }
                 nbar_arrive(BAR_COLS, 32 * ncw);
             }
+            if (GB_NCW > 2 && lane == 31) { sWS[8 * b + warp] = iS; sWQ[8 * b + warp] = iQ; }
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
@@ -1460,7 +1465,12 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
                 cQ[j] = cQ[j] + ev * ev - ov * ov;
             }
             uint32_t bS = iS - TS, bQ = iQ - TQ;
-            if (warp == 1) {
+            if (GB_NCW > 2) {
+                nbar_sync(BAR_COLS, 32 * ncw);
+#pragma unroll
+                for (int w = 0; w < GB_NCW - 1; ++w)
+                    if (w < warp) { bS += sWS[8 * b + w]; bQ += sWQ[8 * b + w]; }
+            } else if (warp == 1) {
                 nbar_sync(BAR_COLS, 32 * ncw);
                 bS += sWS[8 * b]; bQ += sWQ[8 * b];
             }
@@ -1931,9 +1941,9 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         const int ns = (p.cols + gb_tw - 1) / gb_tw;
         best_strips = ns;
         best_tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
-        best_w = GB_NC / 1024;
+        best_w = GB_NCW;
         p.ncw = best_w;
-        p.now = 2;  // (the role swap below pairs 2 column with 2 output warps)
+        p.now = GB_NCW;  // (the role swap below pairs the two equal halves of the CTA)
         {
             const char* se = getenv("DTB_GB_SWAP");
             p.role_div = (se && atoi(se) > 0) ? atoi(se) : 0;
