@@ -338,9 +338,11 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     const int f_hi = min(X0 + p.TW, p.cols);
     const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
 
+    // warm-up items carry up to 3 warm-up rows each (E, O, F slots), as in gb_kernel
     Items it;
     it.g0 = max(ya - p.r, 0);
-    it.nwarm = min(ya + p.r, p.H - 1) - it.g0 + 1;
+    const int nwr = min(ya + p.r, p.H - 1) - it.g0 + 1;  // warm-up rows
+    it.nwarm = (nwr + 2) / 3;                             // warm-up items
     it.ya = ya;
     it.n = it.nwarm + (yb - ya);
 
@@ -373,7 +375,18 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
         uint8_t* F = O + p.NC;
         int ge, go = -1, gf = -1;
         if (k < it.nwarm) {
-            ge = it.g0 + k;
+            // warm-up rows g0+3k .. g0+3k+2 into the E, O, F slots (full strip width each)
+            if ((!DTB_PAR_PRODUCER || which == 0)) {
+                const uint32_t rowb = (uint32_t)(c_hi16 - c_lo);
+                const int g = it.g0 + 3 * k, cnt = min(3, it.g0 + nwr - g);
+                mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
+                for (int i = 0; i < cnt; ++i) {
+                    uint8_t* D = E + i * p.NC;
+                    if (rowb) bulk_g2s(D + (c_lo - xc0), row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
+                    for (int c = c_hi16; c < c_hi; ++c) D[c - xc0] = row_at<SEG>(p, in0, g + i)[c];
+                }
+            }
+            return;
         } else {
             const int y = it.ya + (k - it.nwarm);
             gf = y;
@@ -456,18 +469,21 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     for (int k = 0; k < it.nwarm; ++k) {
         const int s = k % NS;
         mbar_wait(&full[s], (k / NS) & 1);
-        const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + V * t);
-        uint32_t w[V / 4];
+        const int cnt = min(3, nwr - 3 * k);
+        for (int i = 0; i < cnt; ++i) {
+            const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + i * p.NC + V * t);
+            uint32_t w[V / 4];
 #pragma unroll
-        for (int q = 0; q < V / 16; ++q) {
-            const uint4 a = E[q];
-            w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
-        }
+            for (int q = 0; q < V / 16; ++q) {
+                const uint4 a = E[q];
+                w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+            }
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const uint32_t v = byte_at(w, j);
-            cS[j] += v;
-            cQ[j] += v * v;
+            for (int j = 0; j < V; ++j) {
+                const uint32_t v = byte_at(w, j);
+                cS[j] += v;
+                cQ[j] += v * v;
+            }
         }
         release(k);
         if (producer && k + NS - 1 < it.n) issue(k + NS - 1, lane);
@@ -753,9 +769,11 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
     const int c_hi16 = c_lo + ((max(c_hi - c_lo, 0)) & ~15);
     const int f_hi = min(X0 + p.TW, p.cols);
     const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
+    // warm-up items carry up to 3 warm-up rows each (E, O, F slots), as in gb_kernel
     Items it;
     it.g0 = max(ya - p.r, 0);
-    it.nwarm = min(ya + p.r, p.H - 1) - it.g0 + 1;
+    const int nwr = min(ya + p.r, p.H - 1) - it.g0 + 1;  // warm-up rows
+    it.nwarm = (nwr + 2) / 3;                             // warm-up items
     it.ya = ya;
     it.n = it.nwarm + (yb - ya);
 
@@ -782,7 +800,18 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
         uint8_t* F = O + p.NC;
         int ge, go = -1, gf = -1;
         if (k < it.nwarm) {
-            ge = it.g0 + k;
+            // warm-up rows g0+3k .. g0+3k+2 into the E, O, F slots (full strip width each)
+            if (true) {
+                const uint32_t rowb = (uint32_t)(c_hi16 - c_lo);
+                const int g = it.g0 + 3 * k, cnt = min(3, it.g0 + nwr - g);
+                mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
+                for (int i = 0; i < cnt; ++i) {
+                    uint8_t* D = E + i * p.NC;
+                    if (rowb) bulk_g2s(D + (c_lo - xc0), row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
+                    for (int c = c_hi16; c < c_hi; ++c) D[c - xc0] = row_at<SEG>(p, in0, g + i)[c];
+                }
+            }
+            return;
         } else {
             const int y = it.ya + (k - it.nwarm);
             gf = y;
@@ -826,18 +855,21 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
         for (int k = 0; k < it.nwarm; k += helped ? 2 : 1) {
             const int s = k % NS;
             mbar_wait(&full[s], (k / NS) & 1);
-            const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + V * t);
-            uint32_t w[V / 4];
+            const int cnt = min(3, nwr - 3 * k);
+            for (int i = 0; i < cnt; ++i) {
+                const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + i * p.NC + V * t);
+                uint32_t w[V / 4];
 #pragma unroll
-            for (int q = 0; q < V / 16; ++q) {
-                const uint4 a = E[q];
-                w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
-            }
+                for (int q = 0; q < V / 16; ++q) {
+                    const uint4 a = E[q];
+                    w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+                }
 #pragma unroll
-            for (int j = 0; j < V; ++j) {
-                const uint32_t v = byte_at(w, j);
-                cS[j] += v;
-                cQ[j] += v * v;
+                for (int j = 0; j < V; ++j) {
+                    const uint32_t v = byte_at(w, j);
+                    cS[j] += v;
+                    cQ[j] += v * v;
+                }
             }
             __syncwarp();
             // even items: warp 0 also arrives for the output warps; odd items (unhelped warps
@@ -1008,18 +1040,20 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
                 const int s = k % NS;
                 mbar_wait(&full[s], (k / NS) & 1);
                 if (helper) {
-                    const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + V * to);
-                    uint32_t w[V / 4];
+                    for (int i = 0; i < min(3, nwr - 3 * k); ++i) {
+                        const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + i * p.NC + V * to);
+                        uint32_t w[V / 4];
 #pragma unroll
-                    for (int q = 0; q < V / 16; ++q) {
-                        const uint4 a = E[q];
-                        w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
-                    }
+                        for (int q = 0; q < V / 16; ++q) {
+                            const uint4 a = E[q];
+                            w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+                        }
 #pragma unroll
-                    for (int j = 0; j < V; ++j) {
-                        const uint32_t v = byte_at(w, j);
-                        hS[j] += v;
-                        hQ[j] += v * v;
+                        for (int j = 0; j < V; ++j) {
+                            const uint32_t v = byte_at(w, j);
+                            hS[j] += v;
+                            hQ[j] += v * v;
+                        }
                     }
                 }
                 __syncwarp();
@@ -1525,7 +1559,6 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
         const bool border_warp = __any_sync(0xffffffffu, has_out && !x_interior);
         const int qB = (ALPHA + 2 * p.r + 1) >> 5;  // lane offset of the B streams
         const int qB3 = (ALPHA + 2 * p.r + 4) >> 5;
-        const int a_word = ALPHA + 32 * to, b_word = ALPHA + 2 * p.r + 1 + 32 * to;
         const float W = (float)(2 * p.r + 1);
         const float a1 = p.a, cK = p.c;  // 1-k, k/R
         const float kUp = 1.0f + 7.62939453125e-6f, kDn = 1.0f - 7.62939453125e-6f;  // 1 +- 2^-17
