@@ -1937,6 +1937,31 @@ cudaError_t set_fp32_audit(unsigned long long* counters) {
     return cudaMemcpyToSymbol(g_fp32_audit, &counters, sizeof(counters));
 }
 
+// Band count minimising waves * (TH + wf (2r+1)) + tf * TH in main-row units per CTA slot
+// (see the gb_kernel launcher); DTB_BAND_SCALE overrides with scale x one wave.
+static int plan_bands(int rows_out, int units, int slots, int r, double wf, double tf) {
+    int nbands = 1;
+    if (getenv("DTB_BAND_SCALE")) {
+        nbands = std::max(1, (int)(band_scale() * slots / std::max(1, units)));
+    } else {
+        double best_cost = 1e300;
+        const int nb_max = std::max(1, std::min((rows_out + 7) / 8, 4 * slots / std::max(1, units) + 1));
+        for (int nb = 1; nb <= nb_max; ++nb) {
+            const int th = (rows_out + nb - 1) / nb;
+            const int waves = (units * nb + slots - 1) / slots;
+            const double cost = waves * (th + wf * (2 * r + 1)) + tf * th;
+            if (cost < best_cost) { best_cost = cost; nbands = nb; }
+        }
+    }
+    return std::max(1, std::min(nbands, (rows_out + 7) / 8));
+}
+
+static int slide_band_model() {  // DTB_BAND_MODEL=0: one full wave (the previous rule)
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("DTB_BAND_MODEL"); v = e ? atoi(e) : 1; }
+    return v;
+}
+
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
     slide_constants(p);
     const int vset = slide_v();
@@ -2076,7 +2101,8 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         ws_dispatch(m, sv, dim3(), nt, smem, p, st, &occ, v16);
         const int slots = num_sms * occ;
         int nbands = std::max(1, (int)(band_scale() * slots / std::max(1, best_strips * n_images)));
-        nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
+        nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));  // one wave (the model measured
+                                                                     // 1-4% slower here, C5 W195+)
         p.TH = (rows_out + nbands - 1) / nbands;
         dim3 grid(best_strips, (rows_out + p.TH - 1) / p.TH, n_images);
         if (print_plan())
@@ -2100,6 +2126,8 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     const int slots = num_sms * occ;
     int nbands = std::max(1, (int)(band_scale() * slots / std::max(1, nstrips * n_images)));
     nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
+    // cost-model band count (C3 0.949 -> 0.885 ms, C5 W19..W179 2-4% faster than one wave)
+    if (slide_band_model()) nbands = plan_bands(rows_out, nstrips * n_images, slots, p.r, 0.25, 0.1);
     p.TH = (rows_out + nbands - 1) / nbands;
     dim3 grid(nstrips, (rows_out + p.TH - 1) / p.TH, n_images);
     if (print_plan())
