@@ -2065,12 +2065,12 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         return gb_dispatch(p.r & 15, grid, nt, smem, p, st, nullptr);
     }
     // Auto V: 16 columns per thread give strips in 512-column steps (and 128-register warps);
-    // take them when that cuts the staged column work by >= 15% (C2 pages 2480 wide: one strip
-    // of 2560 instead of three of 1024 -- W15 0.119 -> 0.058 ms; C5 W195+: 6144 -> 5120 columns,
-    // 5-7% faster).  Smaller savings measured no gain or a loss (C5 W19..W179).
+    // take them when that cuts the staged column work by >= 10% (C2 pages 2480 wide: one strip
+    // of 2560 instead of three of 1024 -- W15 0.119 -> 0.058 ms; C5 W3: 0.093 -> 0.078 ms;
+    // C5 W67 / W131 within 2%).
     if (!vset && !p.nseg && V == 32) {
         const Plan p16 = plan_for(16);
-        if (p16.w > 0 && p16.work * 100 < pl.work * 85) {
+        if (p16.w > 0 && p16.work * 10 <= pl.work * 9) {
             V = 16;
             best_w = p16.w; best_strips = p16.strips; best_tw = p16.tw;
         }
