@@ -1775,6 +1775,14 @@ static cudaError_t dispatch_rx(int m, bool sv, dim3 grid, int nt, size_t smem,
     return cudaErrorInvalidValue;
 }
 
+// DTB_PLAN_TIE=1: on equal staged work prefer more column warps per strip (fewer strips);
+// measured neutral (C3 -1%, C5 W163/W179 +4%), so the default keeps the narrowest plan
+static bool plan_tie_wide() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("DTB_PLAN_TIE"); v = e ? atoi(e) : 0; }
+    return v == 1;
+}
+
 // DTB_SLIDE_V=16 / 32 forces the columns per thread of the sliding kernels; unset = auto
 static int slide_v() {
     static int v = -1;
@@ -1980,7 +1988,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
             const int ns = (p.cols + twmax - 1) / twmax;
             const int tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
             const long work = (long)ns * nc;
-            if (b.w == 0 || work < b.work) b = Plan{w, ns, tw, work};
+            if (b.w == 0 || work < b.work || (plan_tie_wide() && work == b.work)) b = Plan{w, ns, tw, work};
         }
         return b;
     };
