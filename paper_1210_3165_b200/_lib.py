@@ -52,6 +52,8 @@ SIGNATURES = {
                     _c_p, _c_i64, _c_i32, _c_f64, _c_f64, _c_p],
     "dtb_set_fp32_audit": [_c_p],
     "dtb_last_kernel": [],
+    "dtb_debug_bb_exact": [_c_p, _c_i32],
+    "dtb_debug_bb_times": [_c_p, _c_i32],
     "dtb_confusion": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
     "dtb_sweep_counts": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p,
                          _c_i32, _c_i32, _c_f64, _c_p, _c_p],

@@ -1,0 +1,743 @@
+// dtb_block.cu -- block-sum group-bound Sauvola kernel (bb_kernel), sm_100a.
+//
+// Replaces, for the binary output of Sauvola with 0 < k <= 1, the reference chain
+// threshold.py:121-148 -> stats.py:171-191 (window sums) -> stats.py:50-54 (_finish_arrays)
+// -> threshold.py:143-147 (t = mean*(1 + k*(std/R - 1)), binary = f < t ? 0 : 255), bit for bit.
+//
+// Work per pixel is the point of this kernel (the path is issue-bound on CUDA cores, not
+// HBM-bound): the column side keeps only 4-column BLOCK sums, the output side decides 8
+// pixels at a time from bounds, and the exact per-pixel sums are rebuilt only for the rare
+// groups the bounds cannot decide.
+//
+// Layout.  A CTA owns a strip of NC = 1024*NCW staged image columns [xc0, xc0+NC)
+// (xc0 = X0 - r - alpha = 0 mod 16) and a band of output rows; it outputs columns
+// [X0, X0+TW).  Strip column i lies in block i/4 (NB = NC/4 blocks).
+//  * Column warps: lane q keeps, for its 8 blocks (strip bytes 32q..32q+31), the exact block
+//    sums BS = sum f, BQ = sum f^2 over rows [y-r, y+r] (clipped) -- two dp4a per 4 columns
+//    for the entering row and two for the leaving row.  Per row they publish the exclusive
+//    block prefix P[b] = sum of blocks < b (uint32, exact mod 2^32) split in an even and an
+//    odd plane (one STS.128 per plane per lane), double buffered.
+//  * Output warps: a group is 8 output pixels X0+8g..X0+8g+7.  With the block-aligned
+//    intersection I' (blocks inside every pixel's window) and union U' (blocks covering
+//    every pixel's window) of the group's 8 windows:
+//        S_I' <= S(x) <= S_U'       for every pixel x of the group
+//    and for ANY integer c, Sum_X (f-c)^2 >= n var(x) and X subset of U', so
+//        n var(x) <= E = Q_U' - 2 c S_U' + n_U c^2      (exact in uint32: E < 2^32)
+//    with c = floor(S_I'/n) (close to the mean, which keeps the bound tight).  Sauvola's
+//    t = m (1-k) + (k/R) m s is nondecreasing in m and s (0 < k <= 1), so
+//        t_lo = m_lo (1-k)                   m_lo = S_I'/n_max
+//        t_hi = m_hi ((1-k) + (k/R) sqrt(E/n_min))   m_hi = S_U'/n_min
+//    evaluated in fp32 with directed slack (relative 2^-17 per factor + the certified
+//    tolerance `tol`, which also covers the reference's own fp64 rounding).  A pixel with
+//    f < ceil(t_lo) is black, one with f >= ceil(t_hi) white (f is an integer); the compare
+//    is a SWAR on 16-bit lanes.  All prefix reads of a warp are consecutive words.
+//  * Uncertain groups (some pixel with ceil(t_lo) <= f < ceil(t_hi); ~1e-5 of groups on the
+//    BASELINE C4 page) are re-decided exactly by the whole warp: lanes sum the <= 2 x 11
+//    edge columns the blocks do not cover straight from the image rows (global / L2), exact
+//    S, Q per pixel = block part + edge columns, then the certified fp32 decision and the
+//    reference fp64 replay (dtb_common.cuh) within tol.
+//  * Row staging: one producer lane issues cp.async.bulk copies of the entering, leaving and
+//    centre row segments into an NS-stage ring (mbarrier complete_tx); the READY/FREE
+//    hand-off between column and output warps uses named barriers.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "docthresh_b200.h"
+#include "dtb_common.cuh"
+#include "dtb_slide.cuh"
+#include "dtb_async.cuh"
+
+namespace dtb {
+
+#ifndef BB_STAGES
+#define BB_STAGES 3  // ring depth per warp (the warp refills a slot right after consuming it)
+#endif
+#ifndef BB_GPL
+#define BB_GPL (BB_NC_DEF / 256)  // group slots per lane (groups of 8 output columns)
+#endif
+
+
+// words of one prefix plane: entries P[2m] (even) or P[2m+1] (odd), m <= NB/2, 16-byte padded
+__host__ __device__ constexpr int bb_plane_words(int NB) { return ((NB / 2 + 1) + 3) & ~3; }
+
+#ifndef BB_NC_DEF
+#define BB_NC_DEF 1024
+#endif
+constexpr int BB_NC = BB_NC_DEF;                  // staged strip columns per warp
+constexpr int BB_NB = BB_NC / 4;                  // 4-column blocks
+constexpr int BB_BPL = BB_NB / 32;                // blocks per lane (column side)
+constexpr int BB_PLW = bb_plane_words(BB_NB);
+// per-warp shared memory: ring NS x (E, O, F) x NC bytes, 4 prefix planes, NS mbarriers
+constexpr int BB_WARP_BYTES = ((BB_STAGES * 3 * BB_NC + 16 * BB_PLW + 8 * BB_STAGES) + 127) & ~127;
+
+
+// fp32-epilogue audit counters (dtb_set_fp32_audit), this translation unit's copy
+__device__ unsigned long long* g_bb_audit = nullptr;
+// number of groups re-decided by the exact path since the last dtb_debug_bb_exact() read
+__device__ unsigned long long g_bb_nexact = 0;
+// debug (dtb_debug_bb_times): when set, CTA i writes its %globaltimer start / end to [2i], [2i+1]
+__device__ unsigned long long* g_bb_times = nullptr;
+__device__ int g_bb_times_cap = 0;
+__device__ __forceinline__ unsigned long long bb_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ceil(x) for x in (-0.5, 2^22) replicated in two 16-bit lanes: FADD.RP onto 2^23 leaves
+// 2^23 + ceil(x); its bit pattern minus 0x4B000000 is ceil(x).
+__device__ __forceinline__ uint32_t bb_ceil2(float x) {
+    const uint32_t bits = __float_as_uint(__fadd_ru(x, 8388608.0f));
+    return bits * 0x10001u - 0x4B000000u * 0x10001u;
+}
+
+// P[bi] of one prefix array (even / odd planes PLW words apart)
+__device__ __forceinline__ uint32_t bb_pre(const uint32_t* A, int bi) {
+    return A[(bi & 1) * BB_PLW + (bi >> 1)];
+}
+
+// three 32-bit words of image row rp at columns c0, c0+4, c0+8 (c0 = 0 mod 4), zeros outside
+__device__ __forceinline__ void bb_words3(const uint8_t* rp, int c0, int cols, uint32_t (&w)[3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int c = c0 + 4 * i;
+        if (c >= 0 && c + 4 <= cols) {
+            w[i] = __ldg(reinterpret_cast<const uint32_t*>(rp + c));
+        } else {
+            uint32_t v = 0;
+            for (int b = 0; b < 4; ++b)
+                if (c + b >= 0 && c + b < cols) v |= (uint32_t)__ldg(rp + c + b) << (8 * b);
+            w[i] = v;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t bb_sel3(const uint32_t (&w)[3], int i) {
+    return i == 0 ? w[0] : (i == 1 ? w[1] : w[2]);
+}
+
+// Exact re-decision of group g (8 pixels) of output row y by the whole warp.  A pixel's window
+// [a, a+2r] (strip columns, a = alpha+8g+j) is its block part [4 blo, 4 bhi) from the prefix plus
+// a partial word on each side: bytes (a&3).. of the word holding a, and bytes ..(a+2r)&3 of the
+// word at 4 bhi.  Lanes take the window rows 32 apart and accumulate those partial words with
+// dp4a; a butterfly sums them; lane j finishes pixel j (certified fp32 decision, fp64 replay
+// within tol).  Returns the group's two output words (every lane).
+template <bool SEG>
+__device__ __forceinline__ uint2 bb_exact_group(const SlideParams* pp, const uint8_t* in0,
+                                             const uint32_t* PS, const uint32_t* PQ,
+                                             const uint8_t* F, int g, int y, int X0, int xc0,
+                                             int alpha, int ny) {
+    const SlideParams& p = *pp;
+    const int lane = threadIdx.x & 31;
+    const int r = p.r;
+    if (lane == 0) atomicAdd(&g_bb_nexact, 1ull);
+    const int a0 = alpha + 8 * g;
+    const int baseL = a0 & ~3;
+    const int baseR = (a0 + 2 * r + 1) & ~3;
+    uint32_t S[8], Q[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { S[j] = 0; Q[j] = 0; }
+    const int r0 = max(y - r, 0), r1 = min(y + r, p.H - 1);
+    // rows r0 + lane + 32 m: all loads of a 4-row batch are in flight together
+    for (int rb = r0 + lane; rb - lane <= r1; rb += 128) {
+        uint32_t wl[4][3], wr[4][3];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int row = rb + 32 * m;
+            if (row <= r1) {
+                const uint8_t* rp = row_at<SEG>(p, in0, row);
+                bb_words3(rp, xc0 + baseL, p.cols, wl[m]);
+                bb_words3(rp, xc0 + baseR, p.cols, wr[m]);
+            } else {
+                wl[m][0] = wl[m][1] = wl[m][2] = wr[m][0] = wr[m][1] = wr[m][2] = 0;
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int a = a0 + j, b = a + 2 * r + 1;  // window [a, b)
+                const int lo = a & 3, hi = b & 3;
+                const uint32_t ml = lo ? (0xFFFFFFFFu << (8 * lo)) : 0u;
+                const uint32_t mr = hi ? (0xFFFFFFFFu >> (32 - 8 * hi)) : 0u;
+                const uint32_t xl = bb_sel3(wl[m], (a - baseL) >> 2) & ml;
+                const uint32_t xr = bb_sel3(wr[m], ((b & ~3) - baseR) >> 2) & mr;
+                S[j] = __dp4a(xl, 0x01010101u, __dp4a(xr, 0x01010101u, S[j]));
+                Q[j] = __dp4a(xl, xl, __dp4a(xr, xr, Q[j]));
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            S[j] += __shfl_xor_sync(0xffffffffu, S[j], off);
+            Q[j] += __shfl_xor_sync(0xffffffffu, Q[j], off);
+        }
+    }
+    uint32_t Sx = 0, Qx = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (lane == j) { Sx = S[j]; Qx = Q[j]; }
+    uint32_t white = 0;
+    if (lane < 8) {
+        const int a = a0 + lane;
+        const int blo = (a + 3) >> 2, bhi = (a + 2 * r + 1) >> 2;
+        Sx += bb_pre(PS, bhi) - bb_pre(PS, blo);
+        Qx += bb_pre(PQ, bhi) - bb_pre(PQ, blo);
+        const int x = X0 + 8 * g + lane;
+        if (x < p.cols) {
+            const uint32_t f = F[8 * g + lane];
+            const int nx = min(x + r, p.cols - 1) - max(x - r, 0) + 1;
+            const uint32_t n = (uint32_t)(ny * nx);
+            const float d = fast_diff<DTB_METHOD_SAUVOLA, true>(Sx, Qx, f, n, p.cA, p.cC, p.a, p.c);
+            if (fabsf(d) >= p.tol) {
+                white = d < 0.f ? 0u : 0xFFu;
+            } else {
+                white = exact_white(Sx, Qx, (double)n, f, DTB_METHOD_SAUVOLA, p.k, p.rr);
+                if (unsigned long long* audit = g_bb_audit) {
+                    atomicAdd(&audit[0], 1ull);
+                    if (white != (d < 0.f ? 0u : 0xFFu)) {
+                        double mean, sd;
+                        finish_exact((double)Sx, (double)Qx, (double)n, mean, sd);
+                        const double tt = threshold_exact(mean, sd, DTB_METHOD_SAUVOLA, p.k, p.rr);
+                        atomicAdd(&audit[1], 1ull);
+                        atomicMax(&audit[2], (unsigned long long)__float_as_uint((float)fabs((double)f - tt)));
+                    }
+                }
+            }
+        }
+    }
+    uint32_t v = white << (8 * (lane & 3));
+    v |= __shfl_xor_sync(0xffffffffu, v, 1);
+    v |= __shfl_xor_sync(0xffffffffu, v, 2);
+    return make_uint2(__shfl_sync(0xffffffffu, v, 0), __shfl_sync(0xffffffffu, v, 4));
+}
+
+// Per-pixel bounds for the pixel at image column x (strip column a = start of its window):
+// its own block-aligned windows (blocks inside / covering [a, a+2r]: at most 3 columns of slack
+// per side) and its own clipped count, with the centred variance bounds of the group test.
+// Returns 0 (black), 0xFF (white) or -1 (still open: the exact path decides).
+__device__ __forceinline__ int bb_pixel_decide(const uint32_t* PS, const uint32_t* PQ, uint32_t f, int a, int x,
+                                            int xc0, int cols, int r, int ny, float a_up, float a_dn,
+                                            float cK_up, float cK_dn, float tol) {
+    const float kUp = 1.0f + 7.62939453125e-6f, kDn = 1.0f - 7.62939453125e-6f;
+    const int b = a + 2 * r + 1;
+    const int il = (a + 3) >> 2, ih = b >> 2, ul = a >> 2, uh = (b + 3) >> 2;
+    const uint32_t sI = bb_pre(PS, ih) - bb_pre(PS, il), sU = bb_pre(PS, uh) - bb_pre(PS, ul);
+    const uint32_t qI = bb_pre(PQ, ih) - bb_pre(PQ, il), qU = bb_pre(PQ, uh) - bb_pre(PQ, ul);
+    const int cu = min(xc0 + 4 * uh, cols) - max(xc0 + 4 * ul, 0);  // in-image columns of U', I'
+    const int ci = max(min(xc0 + 4 * ih, cols) - max(xc0 + 4 * il, 0), 0);
+    const uint32_t nU = (uint32_t)(ny * cu), nI = (uint32_t)(ny * ci);
+    const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
+    const float rn = rcp_ftz((float)(ny * nx)), rlo = rn * kUp, rhi = rn * kDn;
+    const float mlo = (float)sI * rhi, mhi = (float)sU * rlo;
+    const uint32_t c = __float2uint_rz(mlo);
+    const uint32_t E = qU + c * (nU * c - 2u * sU);
+    const float thi = __fmaf_rn(mhi, __fmaf_rn(sqrt_ftz((float)E * rlo), cK_up, a_up), tol);
+    float slo = 0.f;
+    if (nI > 0) {
+        const uint32_t EI = qI + c * (nI * c - 2u * sI);
+        const float d = (float)(int)(sI - nI * c);
+        const float v = __fmaf_rn(-(d * d) * kUp, rcp_ftz((float)nI) * kUp, (float)EI * kDn);
+        slo = sqrt_ftz(fmaxf(v, 0.f) * rhi) * kDn;
+    }
+    const float tlo = __fmaf_rn(mlo, __fmaf_rn(slo, cK_dn, a_dn), -tol);
+    const float ff = (float)f;
+    return ff < tlo ? 0 : (ff >= thi ? 0xFF : -1);
+}
+
+// An interior group the group bounds left open: per-pixel bounds for its 8 pixels.  Rewrites
+// the decided bytes of (o0, o1); returns whether some pixel is still open.
+__device__ __forceinline__ bool bb_pixel_refine(const uint32_t* PS, const uint32_t* PQ, uint2 fv, int a0, int x0,
+                                                int xc0, int cols, int r, int ny, float a_up, float a_dn,
+                                                float cK_up, float cK_dn, float tol, uint32_t& o0, uint32_t& o1) {
+    bool open = false;
+    uint32_t ob[2] = {o0, o1};
+#pragma unroll 1
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t sh = 8 * (j & 3);
+        const int v = bb_pixel_decide(PS, PQ, ((j < 4 ? fv.x : fv.y) >> sh) & 0xFFu, a0 + j, x0 + j, xc0, cols,
+                                      r, ny, a_up, a_dn, cK_up, cK_dn, tol);
+        if (v < 0) open = true;
+        else ob[j >> 2] = (ob[j >> 2] & ~(0xFFu << sh)) | ((uint32_t)v << sh);
+    }
+    o0 = ob[0];
+    o1 = ob[1];
+    return open;
+}
+
+__device__ __forceinline__ bool bb_elect() {
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n}" : "=r"(e));
+    return e != 0;
+}
+
+// One CTA = one warp = one pipeline: a strip of BB_NC staged columns x a band of output rows of
+// one image.  blockIdx.x -> (strip, band, image), strips fastest.  Every control value is
+// warp-uniform; lane 0 (elected) issues the bulk copies.
+template <bool SEG, int MINB>
+__global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ SlideParams p,
+                                                      int nstrips, int nbands, int tw0) {
+    constexpr int NS = BB_STAGES, NC = BB_NC, NB = BB_NB, PLW = BB_PLW;
+    extern __shared__ __align__(128) uint8_t smb[];
+    uint8_t* ring = smb;
+    uint32_t* PSe = reinterpret_cast<uint32_t*>(smb + NS * 3 * NC);
+    uint32_t* PQe = PSe + 2 * PLW;
+    uint64_t* full = reinterpret_cast<uint64_t*>(PSe + 4 * PLW);
+    const int lane = threadIdx.x;
+    const int pid = blockIdx.x;
+    unsigned long long* const tdbg = (g_bb_times && pid < g_bb_times_cap) ? g_bb_times + 4 * pid : nullptr;
+    if (tdbg && lane == 0) { tdbg[2] = 0; tdbg[3] = 0; }
+    if (tdbg && lane == 0) tdbg[0] = bb_gtimer();
+    const int strip = pid % nstrips, rest = pid / nstrips;
+    const int band = rest % nbands, img = rest / nbands;
+    const int r = p.r;
+    const int alpha = (16 - (r & 15)) & 15;
+    // strip widths: the first strip tw0 (narrower: its edge groups cost per-pixel bounds), the
+    // others TW (the last one clipped by the image)
+    const int X0 = strip == 0 ? 0 : tw0 + (strip - 1) * p.TW;
+    const int TWs = strip == 0 ? tw0 : p.TW;
+    const int xc0 = X0 - r - alpha;
+    const int ya = p.out_begin + band * p.TH;
+    const int yb = min(ya + p.TH, p.out_end);
+    if (ya >= yb) return;
+    const uint8_t* in0 = p.in + (int64_t)img * p.img_stride - (int64_t)p.row0 * p.pitch;
+    const int c_lo = max(xc0, 0);
+    const int c_hi = min(xc0 + NC, p.cols);
+    const int c_hi16 = c_lo + ((max(c_hi - c_lo, 0)) & ~15);
+    const int f_hi = min(X0 + TWs, p.cols);
+    const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
+    const int g0 = max(ya - r, 0);
+    const int nwr = min(ya + r, p.H - 1) - g0 + 1;  // warm-up rows (3 per item)
+    const int nwarm = (nwr + 2) / 3;
+    const int n_items = nwarm + (yb - ya);
+
+    for (int i = lane; i < NS * 3 * NC / 16; i += 32) reinterpret_cast<uint4*>(ring)[i] = make_uint4(0, 0, 0, 0);
+    if (lane == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zeros before the bulk copies
+    __syncwarp();
+
+    const uint32_t rowb = (uint32_t)(c_hi16 - c_lo), fb = (uint32_t)(f_hi16 - X0);
+    const uint64_t pol_keep = make_policy(2), pol_drop = make_policy(1);
+    const int dE = c_lo - xc0;  // ring offset of column c_lo
+    // item k -> ring slot k % NS: warm-up items carry rows g0+3k.. in the E, O, F slots; row
+    // items the entering row y+r (E), leaving row y-r-1 (O) and centre row y (F, output columns)
+
+    // ---- output-side constants
+    const int NG = TWs / 8;
+    const int iL = (alpha + 10) >> 2, iH = (alpha + 2 * r + 1) >> 2;   // I' = [2g+iL, 2g+iH)
+    const int uL = alpha >> 2, uH = (alpha + 2 * r + 11) >> 2;         // U' = [2g+uL, 2g+uH)
+    // per-stream prefix pointers for this lane's first group (g = lane); slot i adds 32 words
+    const uint32_t* pSiH = PSe + (iH & 1) * PLW + (iH >> 1) + lane;
+    const uint32_t* pSiL = PSe + (iL & 1) * PLW + (iL >> 1) + lane;
+    const uint32_t* pSuH = PSe + (uH & 1) * PLW + (uH >> 1) + lane;
+    const uint32_t* pSuL = PSe + (uL & 1) * PLW + (uL >> 1) + lane;
+    const int W = 2 * r + 1;
+    const uint32_t nUc = 4u * (uint32_t)(uH - uL), nIc = 4u * (uint32_t)(iH - iL);
+    const float kUp = 1.0f + 7.62939453125e-6f, kDn = 1.0f - 7.62939453125e-6f;  // 1 +- 2^-17
+    const float a_up = p.a * kUp, a_dn = p.a * kDn, cK_up = p.c * kUp, cK_dn = p.c * kDn, tol = p.tol;
+    const bool vec_ok = (((uintptr_t)p.bin | (uintptr_t)p.bin_pitch | (uintptr_t)p.out_stride) & 7) == 0;
+    // group slots of this lane: imask = interior groups (all 8 windows inside the image in x)
+    uint32_t imask = 0;
+    // (uniform) valid groups ngv; left-edge groups [0, gl), right-edge groups [gr, ngv)
+    const int ngv = min(TWs / 8, (p.cols - X0 + 7) / 8);
+    const int gl = min(ngv, max(0, (r - X0 + 7) / 8));
+    const int vr = p.cols - 7 - r - X0;  // right-edge groups: X0 + 8g >= vr
+    const int gr = max(gl, min(ngv, vr > 0 ? (vr + 7) / 8 : -((-vr) / 8)));
+    const bool edge_strip = gl > 0 || gr < ngv;
+#pragma unroll
+    for (int i = 0; i < BB_GPL; ++i) {
+        const int g = lane + 32 * i, x0 = X0 + 8 * g;
+        if (g < TWs / 8 && x0 < p.cols) {
+            if (x0 - r >= 0 && x0 + 7 + r <= p.cols - 1) imask |= 1u << i;
+        }
+    }
+    uint8_t* obase = p.bin + (int64_t)img * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
+    const float rnW = 1.0f / (float)(W * W);  // interior rows: n = W^2
+
+    uint32_t bS[BB_BPL], bQ[BB_BPL];
+#pragma unroll
+    for (int j = 0; j < BB_BPL; ++j) { bS[j] = 0; bQ[j] = 0; }
+    // one issue site: iteration k first refills the slot item k-1 left (item k+NS-1), then
+    // consumes item k; the first NS-1 iterations only fill the ring
+    for (int k = 1 - NS; k < n_items; ++k) {
+        if (k + NS - 1 < n_items) do {
+            const int kk = k + NS - 1;
+            const int s = kk % NS;
+            uint8_t* E = ring + s * 3 * NC;
+            if (kk < nwarm) {
+                const int g = g0 + 3 * kk, cnt = min(3, g0 + nwr - g);
+                if (bb_elect()) {
+                    mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
+                    for (int i = 0; i < cnt; ++i)
+                        if (rowb) bulk_g2s(E + i * NC + dE, row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
+                }
+                if (c_hi16 < c_hi) {  // ragged right edge: the last < 16 columns byte by byte
+                    for (int i = 0; i < cnt; ++i)
+                        for (int c = c_hi16 + lane; c < c_hi; c += 32) E[i * NC + c - xc0] = row_at<SEG>(p, in0, g + i)[c];
+                }
+                break;
+            }
+            const int y = ya + (kk - nwarm);
+            const bool fst = (kk == nwarm);
+            const int ge = (fst || y + r >= p.H) ? -1 : y + r;
+            const int go = fst ? -1 : y - r - 1;
+            if (bb_elect()) {
+                mbar_expect_tx(&full[s], fb + (ge >= 0 ? rowb : 0u) + (go >= 0 ? rowb : 0u));
+                if (ge >= 0 && rowb) bulk_g2s(E + dE, row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
+                if (go >= 0 && rowb) bulk_g2s(E + NC + dE, row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+                if (fb) bulk_g2s(E + 2 * NC, row_at<SEG>(p, in0, y) + X0, fb, &full[s], pol_keep);
+            }
+            if (c_hi16 < c_hi || f_hi16 < f_hi) {
+                for (int c = c_hi16 + lane; c < c_hi; c += 32) {
+                    if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
+                    if (go >= 0) E[NC + c - xc0] = row_at<SEG>(p, in0, go)[c];
+                }
+                for (int c = f_hi16 + lane; c < f_hi; c += 32) E[2 * NC + c - X0] = row_at<SEG>(p, in0, y)[c];
+            }
+        } while (0);
+        if (k < 0) continue;
+        const int s = k % NS;
+        mbar_wait(&full[s], (k / NS) & 1);
+        const uint8_t* stage = ring + s * 3 * NC;
+        if (k < nwarm) {
+            const int cnt = min(3, nwr - 3 * k);
+            for (int i = 0; i < cnt; ++i) {
+                const uint4* R = reinterpret_cast<const uint4*>(stage + i * NC + 4 * BB_BPL * lane);
+#pragma unroll
+                for (int h = 0; h < BB_BPL / 4; ++h) {
+                    const uint4 a = R[h];
+                    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        bS[4 * h + j] = __dp4a(w[j], 0x01010101u, bS[4 * h + j]);
+                        bQ[4 * h + j] = __dp4a(w[j], w[j], bQ[4 * h + j]);
+                    }
+                }
+            }
+        } else {
+            const int y = ya + (k - nwarm);
+            const bool fst = (k == nwarm);
+            // ---- column side: block sums, exclusive block prefix -> even / odd planes
+            if (!fst) {
+                const bool ein = y + r < p.H, oin = y - r - 1 >= 0;
+                const uint4* E = reinterpret_cast<const uint4*>(stage + 4 * BB_BPL * lane);
+                const uint4* O = reinterpret_cast<const uint4*>(stage + NC + 4 * BB_BPL * lane);
+                const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int h = 0; h < BB_BPL / 4; ++h) {
+                    const uint4 ev = ein ? E[h] : z, ov = oin ? O[h] : z;
+                    const uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
+                    const uint32_t o[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        bS[4 * h + j] = dp4a_sub(o[j], __dp4a(e[j], 0x01010101u, bS[4 * h + j]));
+                        bQ[4 * h + j] = __dp4a(e[j], e[j], bQ[4 * h + j]) - __dp4a(o[j], o[j], 0u);
+                    }
+                }
+            }
+            {
+                uint32_t TS = 0, TQ = 0;
+#pragma unroll
+                for (int j = 0; j < BB_BPL; ++j) { TS += bS[j]; TQ += bQ[j]; }
+                uint32_t iS = TS, iQ = TQ;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
+                    const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
+                    if (lane >= off) { iS += vs; iQ += vq; }
+                }
+                // lane's exclusive prefix P[16 lane + j]: even j -> even plane, odd j -> odd plane
+                uint32_t vS = iS - TS, vQ = iQ - TQ;
+#pragma unroll
+                for (int h = 0; h < BB_BPL / 8; ++h) {
+                    uint32_t eS[4], oS[4], eQ[4], oQ[4];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        eS[m] = vS; eQ[m] = vQ;
+                        vS += bS[8 * h + 2 * m]; vQ += bQ[8 * h + 2 * m];
+                        oS[m] = vS; oQ[m] = vQ;
+                        vS += bS[8 * h + 2 * m + 1]; vQ += bQ[8 * h + 2 * m + 1];
+                    }
+                    const int w = (BB_BPL / 2) * lane + 4 * h;
+                    *reinterpret_cast<uint4*>(PSe + w) = make_uint4(eS[0], eS[1], eS[2], eS[3]);
+                    *reinterpret_cast<uint4*>(PSe + PLW + w) = make_uint4(oS[0], oS[1], oS[2], oS[3]);
+                    *reinterpret_cast<uint4*>(PQe + w) = make_uint4(eQ[0], eQ[1], eQ[2], eQ[3]);
+                    *reinterpret_cast<uint4*>(PQe + PLW + w) = make_uint4(oQ[0], oQ[1], oQ[2], oQ[3]);
+                }
+                if (lane == 31) {  // P[NB]
+                    PSe[NB / 2] = iS;
+                    PQe[NB / 2] = iQ;
+                }
+            }
+            __syncwarp();
+            // ---- output side: groups of 8 pixels
+            const uint8_t* F = stage + 2 * NC;
+            const int ny = min(y + r, p.H - 1) - max(y - r, 0) + 1;
+            const float rn = (ny == W) ? rnW : rcp_ftz((float)(ny * W));
+            const float rlo = rn * kUp, rhi = rn * kDn;
+            const uint32_t nU = (uint32_t)ny * nUc;
+            uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
+            uint32_t um = 0;
+            // one interior group: bounds -> provisional bytes (stored) -> uncertain flag in um
+            auto group = [&](int i) {
+                const int g = lane + 32 * i;
+                const int x0 = X0 + 8 * g;
+                const uint32_t sI = pSiH[32 * i] - pSiL[32 * i];
+                const uint32_t sU = pSuH[32 * i] - pSuL[32 * i];
+                const uint32_t qU = pSuH[2 * PLW + 32 * i] - pSuL[2 * PLW + 32 * i];
+                const float mlo = (float)sI * rhi;
+                const float mhi = (float)sU * rlo;
+                const uint32_t c = __float2uint_rz(mlo);
+                const uint32_t E = qU + c * (nU * c - 2u * sU);  // sum_{U'} (f - c)^2, exact
+                const float sd = sqrt_ftz((float)E * rlo);
+                const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sd, cK_up, a_up), tol), 4096.f);
+                const uint32_t H2 = bb_ceil2(thi);
+                uint32_t L2 = bb_ceil2(__fmaf_rn(mlo, a_dn, -tol));
+                const uint2 fv = *reinterpret_cast<const uint2*>(F + 8 * g);
+                const uint32_t fA0 = prmt(fv.x, 0x80808080u, 0x4240), fB0 = prmt(fv.x, 0x80808080u, 0x4341);
+                const uint32_t fA1 = prmt(fv.y, 0x80808080u, 0x4240), fB1 = prmt(fv.y, 0x80808080u, 0x4341);
+                const uint32_t wA0 = fA0 - H2, wB0 = fB0 - H2, wA1 = fA1 - H2, wB1 = fB1 - H2;
+                uint32_t o0 = prmt(wA0, wB0, 0xFBD9);  // bytes 0xFF where f >= ceil(t_hi)
+                uint32_t o1 = prmt(wA1, wB1, 0xFBD9);
+                uint32_t u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
+                              ((fB1 - L2) & ~wB1)) & 0x80008000u;
+                if (__builtin_expect(u != 0u, 0)) {
+                    // tighter lower bound: n var(x) >= sum_I' (f - m_I')^2 = E_I - d^2/n_I
+                    const uint32_t qI = pSiH[2 * PLW + 32 * i] - pSiL[2 * PLW + 32 * i];
+                    const uint32_t nI = (uint32_t)ny * nIc;
+                    const uint32_t EI = qI + c * (nI * c - 2u * sI);
+                    const float d = (float)(int)(sI - nI * c);
+                    const float v = __fmaf_rn(-(d * d) * kUp, rcp_ftz((float)nI) * kUp, (float)EI * kDn);
+                    const float slo = sqrt_ftz(fmaxf(v, 0.f) * rhi) * kDn;
+                    L2 = bb_ceil2(__fmaf_rn(mlo, __fmaf_rn(slo, cK_dn, a_dn), -tol));
+                    u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
+                         ((fB1 - L2) & ~wB1)) & 0x80008000u;
+                    if (u && !bb_pixel_refine(PSe, PQe, fv, alpha + 8 * g, x0, xc0, p.cols, r, ny, a_up, a_dn,
+                                              cK_up, cK_dn, tol, o0, o1))
+                        u = 0;
+                }
+                if (u) um |= 1u << i;
+                if (vec_ok) {  // provisional bytes (an uncertain group is rewritten below)
+                    __stcs(reinterpret_cast<uint2*>(orow + x0), make_uint2(o0, o1));
+                } else {
+                    for (int j = 0; j < 8; ++j) orow[x0 + j] = (uint8_t)((j < 4 ? o0 : o1) >> (8 * (j & 3)));
+                }
+            };
+#pragma unroll
+            for (int i = 0; i < BB_GPL; ++i)
+                if ((imask >> i) & 1u) group(i);
+            if (edge_strip) {
+                // groups whose windows the image's left / right edge clips: per-pixel bounds, the
+                // warp's lanes over their pixels (left groups [0, gl), right groups [gr, ngv))
+                const int nbp = 8 * (gl + ngv - gr);
+                for (int q0 = 0; q0 < nbp; q0 += 64) {  // two pixels per lane per pass (ILP)
+                    int v[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int q = q0 + 32 * h + lane;
+                        v[h] = 0x100;  // no pixel
+                        if (q < nbp) {
+                            const int gq = (q >> 3) < gl ? (q >> 3) : gr + (q >> 3) - gl, j = q & 7;
+                            const int x = X0 + 8 * gq + j;
+                            if (x < p.cols)
+                                v[h] = bb_pixel_decide(PSe, PQe, F[8 * gq + j], alpha + 8 * gq + j, x, xc0,
+                                                       p.cols, r, ny, a_up, a_dn, cK_up, cK_dn, tol);
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int q = q0 + 32 * h + lane;
+                        const int gq = (q >> 3) < gl ? (q >> 3) : gr + (q >> 3) - gl, j = q & 7;
+                        if (v[h] != 0x100) orow[X0 + 8 * gq + j] = (uint8_t)(v[h] & 0xFF);
+                        unsigned ob = __ballot_sync(0xffffffffu, v[h] < 0);
+                        while (ob) {  // owners of groups with an open pixel
+                            const int qb = q0 + 32 * h + __ffs(ob) - 1;
+                            ob &= ob - 1;
+                            const int gb = (qb >> 3) < gl ? (qb >> 3) : gr + (qb >> 3) - gl;
+                            if ((gb & 31) == lane) um |= 1u << (gb >> 5);
+                        }
+                    }
+                }
+                __syncwarp();  // the byte stores above precede an owner's exact rewrite below
+            }
+            // uncertain groups: exact per-pixel re-decision, one group at a time by the warp
+            while (__any_sync(0xffffffffu, um != 0u)) {
+                const unsigned bal = __ballot_sync(0xffffffffu, um != 0u);
+                const int src = __ffs(bal) - 1;
+                const int slot = __shfl_sync(0xffffffffu, um ? __ffs(um) - 1 : 0, src);
+                const int g = src + 32 * slot;
+                const uint2 wv = bb_exact_group<SEG>(&p, in0, PSe, PQe, F, g, y, X0, xc0, alpha, ny);
+                if (tdbg && lane == 0) tdbg[2] += 1;
+                if (lane == src) {
+                    um &= ~(1u << slot);
+                    const int x0 = X0 + 8 * g;
+                    if (vec_ok && x0 + 8 <= p.cols) {
+                        __stcs(reinterpret_cast<uint2*>(orow + x0), wv);
+                    } else {
+                        for (int j = 0; j < 8 && x0 + j < p.cols; ++j)
+                            orow[x0 + j] = (uint8_t)((j < 4 ? wv.x : wv.y) >> (8 * (j & 3)));
+                    }
+                }
+            }
+        }
+        __syncwarp();  // every lane is done with slot s (and, for a row, with the prefix)
+    }
+    if (tdbg && lane == 0) tdbg[1] = bb_gtimer();
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+
+// Largest r for which every bound stays exact in uint32: n_U 255^2 < 2^32 with
+// n_U <= (2r+1)(2r+14) (E); the strip must hold the window plus one 16-column step.
+static bool bb_geometry(int r, int& tw) {
+    const int alpha = (16 - (r & 15)) & 15;
+    const int uH = (alpha + 2 * r + 11) >> 2;
+    const int ngmax = std::min((BB_NB - uH) / 2 + 1, 32 * BB_GPL);  // 2(NG-1) + uH <= NB
+    tw = 16 * ((8 * ngmax) / 16);
+    return tw >= 16;
+}
+
+bool bb_eligible(const SlideParams& p) {
+    if (p.method != DTB_METHOD_SAUVOLA || !(p.k > 0.0) || p.k > 1.0) return false;
+    if (p.r < 8 || p.rx != p.r) return false;
+    if ((double)(2 * p.r + 1) * (2 * p.r + 14) * 65025.0 >= 4294967296.0) return false;
+    int tw;
+    return bb_geometry(p.r, tw);
+}
+
+struct BBCache {
+    std::mutex mu;
+    int occ[64][2][2];          // [device][seg][variant] CTAs (= pipelines) per SM (0 = unknown)
+    bool smem_set[64][2][2];    // dynamic-smem opt-in raised
+};
+// register-budget variants: 128 registers (16 pipelines per SM) or 168 (12 per SM)
+static int bb_variant() {
+    const char* e = getenv("DTB_BB_MINB");
+    return (e && atoi(e) == 12) ? 1 : 0;
+}
+static BBCache g_bb;
+
+template <bool SEG, int MINB>
+static cudaError_t bb_prepare(int dev, int* occ) {
+    std::lock_guard<std::mutex> lk(g_bb.mu);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidValue;
+    auto fn = bb_kernel<SEG, MINB>;
+    const int v = MINB == 16 ? 0 : 1;
+    const size_t smem = BB_WARP_BYTES;
+    if (!g_bb.smem_set[dev][SEG][v]) {
+        const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        g_bb.smem_set[dev][SEG][v] = true;
+    }
+    int& o = g_bb.occ[dev][SEG][v];
+    if (!o) {
+        const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32, smem);
+        if (e != cudaSuccess) return e;
+        if (o < 1) o = 1;
+    }
+    *occ = o;
+    return cudaSuccess;
+}
+
+// Band count: the cost per pipeline slot is waves x (TH + wf (2r+1)) + tf TH in main-row units
+// (a warm-up row is two dp4a per 4 columns, ~1/10 of a main row; tf stands for the content-
+// dependent spread of band cost).
+static int bb_plan_bands(int rows_out, int units, int slots, int r) {
+    const double wf = 0.1, tf = 0.1;
+    int best = 1;
+    double best_cost = 1e300;
+    const int nb_max = std::max(1, std::min((rows_out + 7) / 8, 4 * slots / std::max(1, units) + 1));
+    for (int nb = 1; nb <= nb_max; ++nb) {
+        const int th = (rows_out + nb - 1) / nb;
+        const int waves = (units * nb + slots - 1) / slots;
+        const double cost = waves * (th + wf * (2 * r + 1)) + tf * th;
+        if (cost < best_cost) { best_cost = cost; best = nb; }
+    }
+    return std::max(1, std::min(best, (rows_out + 7) / 8));
+}
+
+cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t st, bool print) {
+    slide_constants(p);
+    int tw;
+    if (!bb_geometry(p.r, tw)) return cudaErrorInvalidValue;
+    // Strip plan.  Interior strips output up to tw columns.  The strips holding the image's
+    // left / right edge also decide their edge groups per pixel (~30% more per row on C4), so on
+    // wide pages they get about half a strip: with one wave of pipelines every strip then takes
+    // about as long as the others (C4: the edge strips set the kernel time otherwise).
+    int ns, tw0;
+    if (p.cols >= 4 * tw) {
+        const int e = std::max(16 * ((2 * p.r + 15) / 16), 16 * ((tw / 2 + 15) / 16));
+        const int m = (p.cols - 2 * e + tw - 1) / tw;
+        p.TW = 16 * ((p.cols - 2 * e + 16 * m - 1) / (16 * m));
+        tw0 = e;
+        ns = 1 + (p.cols - tw0 + p.TW - 1) / p.TW;
+    } else {
+        ns = (p.cols + tw - 1) / tw;
+        p.TW = 16 * ((p.cols + 16 * ns - 1) / (16 * ns));  // balanced strips, 16-column steps
+        tw0 = p.TW;
+    }
+    p.NC = BB_NC;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int occ = 1;
+    const int var = bb_variant();
+    e = var ? (p.nseg ? bb_prepare<true, 12>(dev, &occ) : bb_prepare<false, 12>(dev, &occ))
+            : (p.nseg ? bb_prepare<true, 16>(dev, &occ) : bb_prepare<false, 16>(dev, &occ));
+    if (e != cudaSuccess) return e;
+    const int rows_out = p.out_end - p.out_begin;
+    int nbands = bb_plan_bands(rows_out, ns * n_images, num_sms * occ, p.r);
+    if (const char* e = getenv("DTB_BB_BANDS")) nbands = std::max(1, std::min(atoi(e), rows_out));  // A/B
+    p.TH = (rows_out + nbands - 1) / nbands;
+    const int nb = (rows_out + p.TH - 1) / p.TH;
+    const long long np = (long long)ns * nb * n_images;
+    if (np > 0x7fffffffll) return cudaErrorInvalidValue;
+    const int ctas = (int)np;
+    const size_t smem = BB_WARP_BYTES;
+    if (print)
+        fprintf(stderr, "[dtb plan] bb_kernel cols=%d rows=%d r=%d strips=%d TW=%d (first %d) bands=%d TH=%d pipes=%lld ctas=%d occ=%d smem=%zu\n",
+                p.cols, rows_out, p.r, ns, p.TW, tw0, nb, p.TH, np, ctas, occ, smem);
+    set_last_kernel("bb_kernel");
+    if (var) {
+        if (p.nseg) bb_kernel<true, 12><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
+        else bb_kernel<false, 12><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
+    } else {
+        if (p.nseg) bb_kernel<true, 16><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
+        else bb_kernel<false, 16><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t bb_exact_count(unsigned long long* out, bool reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_bb_nexact, sizeof(*out));
+    if (e == cudaSuccess && reset) {
+        const unsigned long long z = 0;
+        e = cudaMemcpyToSymbol(g_bb_nexact, &z, sizeof(z));
+    }
+    return e;
+}
+
+cudaError_t bb_set_times(unsigned long long* buf, int cap) {
+    cudaError_t e = cudaMemcpyToSymbol(g_bb_times, &buf, sizeof(buf));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_bb_times_cap, &cap, sizeof(cap));
+    return e;
+}
+
+cudaError_t set_fp32_audit_block(unsigned long long* counters) {
+    return cudaMemcpyToSymbol(g_bb_audit, &counters, sizeof(counters));
+}
+
+}  // namespace dtb

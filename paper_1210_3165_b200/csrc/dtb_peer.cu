@@ -94,6 +94,19 @@ int dtb_binarize_segments(const uint8_t* const* seg_ptr, const int64_t* seg_pitc
 
 const char* dtb_last_kernel(void) { return dtb::last_kernel(); }
 
+int dtb_debug_bb_times(uint64_t* device_buf, int32_t cap) {
+    const cudaError_t e = dtb::bb_set_times(reinterpret_cast<unsigned long long*>(device_buf), device_buf ? cap : 0);
+    return e == cudaSuccess ? DTB_OK : cuda_fail(e, "dtb_debug_bb_times");
+}
+
+int dtb_debug_bb_exact(uint64_t* count, int32_t reset) {
+    if (!count) return fail(DTB_E_INVALID, "null pointer");
+    unsigned long long v = 0;
+    const cudaError_t e = dtb::bb_exact_count(&v, reset != 0);
+    *count = v;
+    return e == cudaSuccess ? DTB_OK : cuda_fail(e, "dtb_debug_bb_exact");
+}
+
 int dtb_set_fp32_audit(uint64_t* counters3) {
     const cudaError_t e = set_fp32_audit(reinterpret_cast<unsigned long long*>(counters3));
     return e == cudaSuccess ? DTB_OK : cuda_fail(e, "dtb_set_fp32_audit");

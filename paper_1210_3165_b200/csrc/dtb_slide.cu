@@ -38,6 +38,7 @@
 #include "docthresh_b200.h"
 #include "dtb_common.cuh"
 #include "dtb_slide.cuh"
+#include "dtb_async.cuh"
 
 // Tuning switches (measured on B200, C4: quarters 0.662 vs 0.684 ms; a 3-lane producer 0.73 ms)
 #ifndef DTB_PREFIX_QUARTERS
@@ -99,48 +100,13 @@ __device__ __forceinline__ uint32_t byte_at(const uint32_t (&w)[NW], int j) {
     return __byte_perm(w[j >> 2], 0u, 0x4440 | (j & 3));
 }
 
-// prmt.b32 with the raw selector (sign-replicate mode available: nibble bit 3 set copies the
-// sign bit of the selected byte into all 8 bits; __byte_perm masks selectors to 3 bits).
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-    return d;
-}
 
 // padded shared-memory position (in words) of logical chunk L
 __device__ __forceinline__ int pchunk_word(int L) { return 4 * (L + (L >> 3)); }
 
-// DTB_DEBUG_BOUNDS=1: trap on any out-of-range shared-memory index (debug builds; the pool's
-// compute-sanitizer is unavailable, tests/test_fast_path_gpu.py runs once under this build).
-#ifndef DTB_DEBUG_BOUNDS
-#define DTB_DEBUG_BOUNDS 0
-#endif
-#if DTB_DEBUG_BOUNDS
-#define DTB_CHECK(cond)                                                                       \
-    do {                                                                                      \
-        if (!(cond)) {                                                                        \
-            printf("DTB_CHECK failed %s:%d block (%d,%d,%d) thread %d\n", __FILE__, __LINE__, \
-                   blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);                           \
-            __trap();                                                                         \
-        }                                                                                     \
-    } while (0)
-#else
-#define DTB_CHECK(cond) ((void)0)
-#endif
 
 // sqrt_ftz, rcp_ftz, fast_diff, exact_white: dtb_common.cuh
 
-// Address of global row g (in0 = the single buffer's row-0 origin).  Segmented inputs pick
-// the segment holding g; the pointer may be a peer GPU's memory (NVLink), which the bulk
-// copies and loads below read in place.
-// SEG is a compile-time kernel variant: the single-buffer kernels keep the plain address
-// arithmetic (a runtime segment test in the producer's path measured 8% slower on C4).
-template <bool SEG>
-__device__ __forceinline__ const uint8_t* row_at(const SlideParams& p, const uint8_t* in0, int g) {
-    if (!SEG) return in0 + (int64_t)g * p.pitch;
-    const int i = g >= p.seg_lo[2] ? 2 : (g >= p.seg_lo[1] ? 1 : 0);
-    return p.seg_ptr[i] + (int64_t)(g - p.seg_lo[i]) * p.seg_pitch[i];
-}
 
 // fp32-epilogue audit (dtb_set_fp32_audit): when set, the replay path counts
 // [0] pixels replayed in fp64 (|f - t32| < tol), [1] pixels whose plain fp32 sign would have
@@ -254,49 +220,7 @@ __device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t*
     return mind < p.tol;
 }
 
-// ---- asynchronous row staging: cp.async.bulk (TMA engine, no tensor map) + mbarrier
-__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
-    return (uint32_t)__cvta_generic_to_shared(ptr);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1], %2, [%3], %4;"
-        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
-}
-// L2 eviction priorities: a row is read three times (entering, centre r steps later, leaving
-// 2r+1 steps later); keep it resident on the first two reads, let it go on the last.
-__device__ __forceinline__ uint64_t make_policy(int kind) {
-    uint64_t p;
-    if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    else if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
 
-// Sequence of pipeline items for one CTA: warm-up rows g0..g1 (entering row only), then
-// main row steps y = ya..yb-1 (entering row y+r, leaving row y-r-1, centre row y).
-struct Items {
-    int g0, nwarm, ya, n;
-};
 
 // register budget: V=16 fits 128 registers without spills (4 CTAs x 4 warps per SM)
 #ifndef DTB_SLIDE_MINB
@@ -657,41 +581,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
 // be overwritten).  Column warps never wait for the latency-bound output phase of the same
 // row, and output warps never sit behind the column warps' scan / barriers.
 // =====================================================================================
-// Barrier ids are immediates (a register id makes ptxas reserve all 16 barriers, which caps
-// resident CTAs per SM); callers pass (base, buffer) and we branch to constant ids.
-template <int ID>
-__device__ __forceinline__ void nbar_sync_c(int count) {
-    asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(count) : "memory");
-}
-template <int ID>
-__device__ __forceinline__ void nbar_arrive_c(int count) {
-    asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(count) : "memory");
-}
-__device__ __forceinline__ void nbar_sync(int id, int count) {
-    switch (id) {
-        case 1: nbar_sync_c<1>(count); break;
-        case 2: nbar_sync_c<2>(count); break;
-        case 3: nbar_sync_c<3>(count); break;
-        case 4: nbar_sync_c<4>(count); break;
-        case 5: nbar_sync_c<5>(count); break;
-        default: nbar_sync_c<6>(count); break;
-    }
-}
-__device__ __forceinline__ void nbar_arrive(int id, int count) {
-    switch (id) {
-        case 1: nbar_arrive_c<1>(count); break;
-        case 2: nbar_arrive_c<2>(count); break;
-        case 3: nbar_arrive_c<3>(count); break;
-        case 4: nbar_arrive_c<4>(count); break;
-        case 5: nbar_arrive_c<5>(count); break;
-        default: nbar_arrive_c<6>(count); break;
-    }
-}
-__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
-}
 
-enum { BAR_COLS = 1, BAR_READY0 = 2, BAR_FREE0 = 4, BAR_WARM = 6 };
 
 #ifndef DTB_WS_V16_DEFAULT
 #define DTB_WS_V16_DEFAULT 0  // C4: 0.759 ms with V = VO = 16 (24 warps/SM) vs 0.609 with 32 (12)
@@ -1153,12 +1043,6 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
 #define DTB_GB_MAXREG 128
 #endif
 
-// acc - (sum of the four bytes of x): dp4a with unsigned a and signed (-1) b bytes
-__device__ __forceinline__ uint32_t dp4a_sub(uint32_t x, uint32_t acc) {
-    uint32_t d;
-    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(0xFFFFFFFFu), "r"(acc));
-    return d;
-}
 
 #ifndef GB_NCW
 #define GB_NCW 2  // column warps (= output warps) per CTA; NC = 1024 * GB_NCW strip columns
@@ -1942,7 +1826,17 @@ const char* last_kernel() { return g_last_kernel; }
 void set_last_kernel(const char* name) { g_last_kernel = name; }
 
 cudaError_t set_fp32_audit(unsigned long long* counters) {
-    return cudaMemcpyToSymbol(g_fp32_audit, &counters, sizeof(counters));
+    const cudaError_t e = cudaMemcpyToSymbol(g_fp32_audit, &counters, sizeof(counters));
+    return e != cudaSuccess ? e : set_fp32_audit_block(counters);
+}
+
+// DTB_BB: 0 never, 1 whenever eligible, 2 (default) eligible and r >= DTB_BB_MIN_R.
+#ifndef DTB_BB_MIN_R
+#define DTB_BB_MIN_R 24
+#endif
+static int bb_mode() {  // read per launch (tests switch it)
+    const char* e = getenv("DTB_BB");
+    return e ? atoi(e) : 2;
 }
 
 // Band count minimising waves * (TH + wf (2r+1)) + tf * TH in main-row units per CTA slot
@@ -1992,6 +1886,11 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         }
         return b;
     };
+    {
+        const int bbm = bb_mode();
+        if (bbm && bb_eligible(p) && (bbm == 1 || p.r >= DTB_BB_MIN_R))
+            return launch_block(p, n_images, num_sms, st, print_plan());
+    }
     Plan pl = plan_for(V);
     int best_w = pl.w, best_strips = pl.strips, best_tw = pl.tw;
     if (best_w == 0) return cudaErrorInvalidValue;  // window too wide for 8 warps (caller checks)

@@ -1,10 +1,12 @@
-"""Group-bound Sauvola kernel (gb_kernel, dtb_slide.cu) against the CPU oracle, bit-exact.
+"""Block-sum group-bound Sauvola kernel (bb_kernel, dtb_block.cu) against the CPU oracle,
+bit-exact.
 
-The kernel decides 4 adjacent pixels at once from bounds on their window sums and re-decides
-uncertain groups per pixel, so the cases below aim at that split: document pages (almost no
-uncertain groups), uniform noise (many), exact ties (flat windows), every r mod 16 (the
-stream-alignment template), image borders, short images (every row clipped), row bands and
-batches.  DTB_GB=1 forces the kernel wherever it is eligible; dtb_last_kernel() pins that it
+The kernel keeps 4-column block sums, decides 8 adjacent pixels at once from bounds on their
+window sums, and rebuilds exact per-pixel sums for uncertain groups from the image rows.  The
+cases aim at that split: document pages (almost no uncertain groups), uniform noise (most
+groups uncertain), exact ties (flat windows), every r mod 16 (block alignment of the group
+windows), image borders, short images (every row clipped), row bands, segmented inputs and
+batches.  DTB_BB=1 forces the kernel wherever it is eligible; dtb_last_kernel() pins that it
 ran."""
 
 import numpy as np
@@ -17,19 +19,18 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True)
-def force_gb(monkeypatch):
-    monkeypatch.setenv("DTB_GB", "1")
-    monkeypatch.setenv("DTB_BB", "0")  # the block-sum kernel would take these cases first
+def force_bb(monkeypatch):
+    monkeypatch.setenv("DTB_BB", "1")
 
 
-def _ran_gb():
-    return _lib.lib().dtb_last_kernel() == b"gb_kernel"
+def _ran_bb():
+    return _lib.lib().dtb_last_kernel() == b"bb_kernel"
 
 
-def _check(img, win, k, r=128.0, expect_gb=True):
+def _check(img, win, k, r=128.0, expect_bb=True):
     got, _ = engine.binarize(img, win, "sauvola", k, r, want_tmap=False)
-    if expect_gb:
-        assert _ran_gb(), _lib.lib().dtb_last_kernel()
+    if expect_bb:
+        assert _ran_bb(), _lib.lib().dtb_last_kernel()
     want, _ = oracle.binarize(img, win, "sauvola", k, r, tmap=False, threads=8)
     got = got.cpu().numpy()
     if not np.array_equal(got, want):
@@ -39,8 +40,7 @@ def _check(img, win, k, r=128.0, expect_gb=True):
 
 
 def test_c4_crop_w127():
-    img = workloads.c4_image(2048)
-    _check(img, 127, 0.34)
+    _check(workloads.c4_image(2048), 127, 0.34)
 
 
 @pytest.mark.parametrize("rad", range(31, 47))  # every r mod 16
@@ -49,8 +49,8 @@ def test_every_residue(rad):
     _check(img, 2 * rad + 1, 0.34)
 
 
-@pytest.mark.parametrize("rad", [1, 2, 3, 5, 8, 15, 17])
-def test_small_windows_forced(rad):
+@pytest.mark.parametrize("rad", [8, 9, 10, 11, 15, 17, 23, 24, 100, 119, 124])
+def test_window_range(rad):
     img = workloads.doc_gray(257, 2112, rad, 700)
     _check(img, 2 * rad + 1, 0.5)
 
@@ -58,15 +58,15 @@ def test_small_windows_forced(rad):
 @pytest.mark.parametrize("seed", range(4))
 def test_uniform_noise_many_uncertain(seed):
     rng = np.random.default_rng(100 + seed)
-    img = rng.integers(0, 256, (260, 2304)).astype(np.uint8)
-    win = int(rng.choice([63, 65, 99, 127, 201, 255]))
+    img = rng.integers(0, 256, (200, 1808)).astype(np.uint8)
+    win = int(rng.choice([49, 63, 65, 99, 127, 201]))
     k = float(rng.choice([0.05, 0.34, 0.5, 1.0]))
     r = float(rng.choice([128.0, 64.0, 255.0, 1.5]))
     _check(img, win, k, r)
 
 
 def test_flat_windows_exact_ties():
-    # constant 100 and 200 areas: s = 0 -> t = m (1-k) exactly (k = 0.5: t = 100 at m = 200)
+    # constant areas: s = 0 -> t = m (1-k) exactly (k = 0.5: t = 100 at m = 200)
     img = np.full((300, 2208), 200, np.uint8)
     img[:, 1000:1600] = 100
     img[120:180, 300:900] = 0
@@ -81,8 +81,15 @@ def test_short_and_wide_images():
         _check(img, 127, 0.34)
 
 
+def test_narrow_images():
+    # one strip, both image edges inside it; widths just above the radius
+    for w, win in ((80, 63), (128, 127), (160, 99), (256, 201), (896, 127)):
+        img = workloads.doc_gray(180, w, w, 60)
+        _check(img, win, 0.34)
+
+
 def test_right_edge_partial_strip():
-    for w in (1808, 2128, 4112):
+    for w in (912, 1808, 2128, 4112, 16384):
         img = workloads.doc_gray(150, w, w, 300)
         _check(img, 95, 0.34)
 
@@ -95,11 +102,11 @@ def test_bands_and_batch():
     for y0, y1 in ((0, 1), (13, 400), (699, 700), (300, 700)):
         a, z = max(y0 - 63, 0), min(y1 + 63, 700)
         got = engine.binarize_band(dev[a:z], a, 700, y0, y1, 127, "sauvola", 0.34, 128.0)
-        assert _ran_gb()
+        assert _ran_bb()
         assert np.array_equal(got.cpu().numpy(), want[y0:y1]), (y0, y1)
     imgs = np.stack([workloads.doc_gray(256, 2048, s, 300) for s in range(3)])
     got = engine.binarize_batch(torch.from_numpy(imgs).cuda(), 127, "sauvola", 0.34, 128.0)
-    assert _ran_gb()
+    assert _ran_bb()
     for i in range(3):
         assert np.array_equal(got[i].cpu().numpy(),
                               oracle.binarize(imgs[i], 127, "sauvola", 0.34, tmap=False)[0])
@@ -107,18 +114,18 @@ def test_bands_and_batch():
 
 def test_ineligible_falls_back(monkeypatch):
     img = workloads.doc_gray(200, 2112, 9, 300)
-    _check(img, 127, 1.5, expect_gb=False)  # k > 1
-    assert not _ran_gb()
-    got, _ = engine.binarize(img, 127, "niblack", -0.2, 128.0, want_tmap=False)
-    assert not _ran_gb()
-    monkeypatch.setenv("DTB_GB", "0")
-    _check(img, 127, 0.34, expect_gb=False)
-    assert not _ran_gb()
+    _check(img, 127, 1.5, expect_bb=False)  # k > 1
+    assert not _ran_bb()
+    engine.binarize(img, 127, "niblack", -0.2, 128.0, want_tmap=False)
+    assert not _ran_bb()
+    _check(img, 15, 0.34, expect_bb=False)  # r < 8
+    assert not _ran_bb()
+    monkeypatch.setenv("DTB_BB", "0")
+    _check(img, 127, 0.34, expect_bb=False)
+    assert not _ran_bb()
 
 
 def test_segmented_input_matches_page():
-    # dtb_binarize_segments (halo rows in other buffers, e.g. a neighbour GPU's band over
-    # NVLink) on the group-bound kernel's SEG variant
     torch = engine.torch_mod()
     img = workloads.c4_image(2048)[:900, :2048]
     want, _ = oracle.binarize(img, 127, "sauvola", 0.34, tmap=False, threads=8)
@@ -127,26 +134,25 @@ def test_segmented_input_matches_page():
     segs = [(t.data_ptr(), t.stride(0), t.shape[0], t.shape[1]) for t in (top, mid, bot)]
     for y0, y1 in ((263, 637), (0, 900), (640, 900)):
         out = engine.binarize_segments(segs, 0, 900, y0, y1, 127, "sauvola", 0.34, 128.0)
-        assert _ran_gb()
+        assert _ran_bb()
         assert np.array_equal(out.cpu().numpy(), want[y0:y1]), (y0, y1)
 
 
-def test_w257_stays_off_gb():
-    # W = 257 passes the sliding kernels' 2^32 bound but the union window (2r+4 columns)
-    # would not: the group-bound kernel must not run, and a saturated page stays exact
-    img = np.full((600, 2112), 255, np.uint8)
+def test_large_windows_limit():
+    # the uint32 bound E needs (2r+1)(2r+14) 255^2 < 2^32: r <= 124 runs the kernel
+    img = np.full((400, 2112), 255, np.uint8)
     img[::3, ::7] = 254
-    _check(img, 257, 0.34, expect_gb=False)
-    assert not _ran_gb()
-    _check(img, 255, 0.34)  # W = 255 is the largest window the kernel takes
+    _check(img, 249, 0.34)
+    _check(img, 251, 0.34, expect_bb=False)
+    assert not _ran_bb()
 
 
 @pytest.mark.parametrize("seed", range(8))
 def test_random_pages_and_params(seed):
-    rng = np.random.default_rng(2000 + seed)
+    rng = np.random.default_rng(3000 + seed)
     for _ in range(4):
-        h = int(rng.integers(1, 500))
-        w = 16 * int(rng.integers(100, 270))  # 1600..4300 columns, 16-byte rows
+        h = int(rng.integers(1, 400))
+        w = 16 * int(rng.integers(20, 270))
         kind = int(rng.integers(0, 3))
         if kind == 0:
             img = workloads.doc_gray(h, w, int(rng.integers(0, 1 << 30)), max(1, h * w // 3000))
@@ -155,8 +161,8 @@ def test_random_pages_and_params(seed):
         else:  # flat levels + small noise: many near-ties
             base = rng.integers(0, 256, (1, w // 64 + 1)).repeat(64, 1)[:, :w]
             img = np.clip(base + rng.integers(-3, 4, (h, w)), 0, 255).astype(np.uint8)
-        win = int(2 * rng.integers(1, 128) + 1)
+        rad = int(rng.integers(8, 125))
+        rad = min(rad, w - 1)
         k = float(rng.choice([0.01, 0.2, 0.34, 0.5, 0.77, 1.0]))
         r = float(rng.choice([1.0, 16.0, 128.0, 255.0, 300.0]))
-        expect = (2 * (win // 2) + 16 <= 2048) and h > 0
-        _check(img, win, k, r, expect_gb=expect and (win // 2) <= 127)
+        _check(img, 2 * rad + 1, k, r, expect_bb=rad >= 8)
