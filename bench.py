@@ -50,7 +50,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["c4", "c3", "c5", "c2", "c1"], default="c4")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong")
+    ap.add_argument("--emulate-bands", type=int, default=0,
+                    help="one GPU: time one middle band of an N-way row-band split (C4/N) "
+                         "through dtb_binarize_segments; prints its own JSON line")
     ap.add_argument("--window", type=int, default=None, help="override W (c5 sweep point)")
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
                     help="row-band halos: read in place from the neighbours' HBM (CUDA IPC, "
@@ -59,6 +62,36 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
+
+
+def build_id() -> str:
+    """Hash of the kernel sources (csrc + the C-ABI header): ties a committed ncu traffic number
+    to the build it was measured on."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_1210_3165_b200", "csrc", "*.cu*")) +
+                   glob.glob(os.path.join(ROOT, "include", "*.h")))
+    for f in files:
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode() + fh.read())
+    return h.hexdigest()[:16]
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+DTYPE = ("u8 in/out; exact uint32 window sums; decision from certified fp32 bounds "
+         "(8-pixel groups, then per pixel), fp64 reference replay of undecided pixels")
 
 
 def measured_peaks():
@@ -169,6 +202,21 @@ def workload(cfg_name, world, rank, scaling, window):
                     px_rank=rgb.shape[0] * rgb.shape[1], shape=list(rgb.shape),
                     desc=f"c2: 3508x2480 RGB page, fused to_gray + sauvola W={win}")
     raise ValueError(cfg_name)
+
+
+def halo_bytes(w, world) -> int:
+    """Bytes of halo rows all ranks read from their neighbours per step (NVLink)."""
+    if world <= 1:
+        return 0
+    from paper_1210_3165_b200 import distributed as D
+    r = w["win"] // 2
+    rows = w["rows"]
+    total = 0
+    for q in range(world):
+        y0, y1 = D.band_bounds(rows, world, q)
+        a, z = D.halo_bounds(rows, y0, y1, r)
+        total += (y0 - a + z - y1) * w["cols"]
+    return int(total)
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -338,7 +386,10 @@ def run_ours(a):
     if os.path.exists(prof):
         try:
             pt = json.load(open(prof))
-            if pt.get("config") == a.config and pt.get("window") == w["win"]:
+            # only a capture of this very build, config and split counts
+            if (pt.get("config") == a.config and pt.get("window") == w["win"] and
+                    pt.get("build") == build_id() and pt.get("n_gpus", 1) == world and
+                    pt.get("kernel") == kernel_name):
                 traffic = pt.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -358,16 +409,17 @@ def run_ours(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 5),
             "higher_is_better": True,
             "scaling": a.scaling if w["kind"] != "rgb" else "weak",
-            "vs_baseline": None, "dtype": "u8 in/out; int32 sums; f64 epilogue",
+            "vs_baseline": None, "dtype": DTYPE,
             "data": "synthetic (seeded, paper_1210_3165_b200/workloads.py)",
             "config": {"workload": w["desc"], "image": w["shape"], "window": w["win"],
                        "method": w["method"], "k": w["k"], "r": w["r"],
                        "parallelism": f"{'rowband' if w['kind'] == 'rowband' else 'image'}{world}",
-                       **({"halo": w["halo_transport"]} if "halo_transport" in w else {}),
+                       **({"halo": w["halo_transport"],
+                           "halo_bytes_per_step": halo_bytes(w, world)} if "halo_transport" in w else {}),
                        "l2": (f"{nrot} rotating input/output buffer sets, "
                               f"{nrot * per_step_bytes / 2**20:.0f} MiB per rank >= 2x L2 "
                               f"({l2 / 2**20:.0f} MiB)")},
-            "kernel_ms": round(kms, 5), "kernel": kernel_name,
+            "kernel_ms": round(kms, 5), "kernel": kernel_name, "build": build_id(),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
@@ -379,6 +431,85 @@ def run_ours(a):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_band_emulation(a):
+    """One GPU: time one middle band of an N-way row-band split of the page through the
+    segmented-input entry (dtb_binarize_segments), the halo rows in separate buffers exactly
+    as the p2p path maps them from the neighbours, against the whole page in the same
+    process.  Reports ms per band, the linear target (whole page / N) and the efficiency."""
+    import numpy as np
+    import torch
+
+    from paper_1210_3165_b200 import _lib, engine, workloads as wl
+    from paper_1210_3165_b200 import distributed as D
+    nb = a.emulate_bands
+    cfg = wl.CONFIGS[a.config]
+    if a.config not in ("c4", "c5", "c1"):
+        raise SystemExit("--emulate-bands: row-band configs only (c4, c5, c1)")
+    win = a.window or cfg.windows[0]
+    r = win // 2
+    img = {"c4": wl.c4_image, "c5": wl.c5_image, "c1": wl.c1_image}[a.config]()
+    H, Wd = img.shape
+    b = nb // 2  # a middle band: both halos come from neighbours
+    y0, y1 = D.band_bounds(H, nb, b)
+    ha, hz = D.halo_bounds(H, y0, y1, r)
+    dev = torch.device("cuda", 0)
+    props = torch.cuda.get_device_properties(dev)
+    l2 = int(getattr(props, "L2_cache_size", 126 * 2**20))
+    step_bytes = (hz - ha) * Wd + (y1 - y0) * Wd
+    nrot = max(1, -(-2 * l2 // step_bytes))
+    sets = []
+    for _ in range(nrot):
+        top = torch.from_numpy(np.ascontiguousarray(img[ha:y0])).to(dev)
+        mid = torch.from_numpy(np.ascontiguousarray(img[y0:y1])).to(dev)
+        bot = torch.from_numpy(np.ascontiguousarray(img[y1:hz])).to(dev)
+        out = torch.empty((y1 - y0, Wd), dtype=torch.uint8, device=dev)
+        segs = [(t.data_ptr(), t.stride(0), t.shape[0], Wd) for t in (top, mid, bot)]
+        sets.append((segs, out, (top, mid, bot)))
+    page = torch.from_numpy(img).to(dev)
+    pout = torch.empty_like(page)
+    flush = torch.empty(2 * l2, dtype=torch.uint8, device=dev)
+
+    def timed(fn, reps):
+        ts = []
+        for i in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(i)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    def band(i):
+        segs, out, _ = sets[i % nrot]
+        engine.binarize_segments(segs, ha, H, y0, y1, win, cfg.method, cfg.k, cfg.r, out=out)
+
+    def whole(i):
+        engine.binarize(page, win, cfg.method, cfg.k, cfg.r, want_tmap=False, out=pout)
+
+    for i in range(a.warmup):
+        band(i)
+        whole(i)
+    torch.cuda.synchronize()
+    t_band = timed(band, max(5, a.steps))
+    kb = _lib.lib().dtb_last_kernel().decode()
+    t_page = timed(whole, max(5, a.steps))
+    kp = _lib.lib().dtb_last_kernel().decode()
+    ok = np.array_equal(sets[0][1].cpu().numpy(), pout.cpu().numpy()[y0:y1])
+    print(json.dumps({
+        "mode": "band_emulation", "metric": METRIC, "config": a.config, "window": win,
+        "bands": nb, "band": b, "band_rows": [y0, y1], "halo_rows": [ha, y0, y1, hz],
+        "ms_per_band": round(t_band, 5), "band_kernel": kb,
+        "ms_whole_page": round(t_page, 5), "page_kernel": kp,
+        "linear_target_ms": round(t_page / nb, 5),
+        "efficiency": round(t_page / nb / t_band, 4),
+        "emulated_value": round(H * Wd / (t_band / 1e3) / 1e6, 1), "unit": UNIT,
+        "halo_bytes_per_band": int((y0 - ha + hz - y1) * Wd),
+        "band_equals_page_rows": bool(ok),
+        "l2": f"flushed ({2 * l2 >> 20} MiB memset) before every rep"}), flush=True)
 
 
 def run_e2e(a, w, world, rank, local, dev, barrier):
@@ -439,6 +570,8 @@ def run_e2e(a, w, world, rank, local, dev, barrier):
     torch.cuda.synchronize()
     barrier()
     ms = t0.elapsed_time(t1) / steps
+    from paper_1210_3165_b200 import _lib as _dl
+    e2e_kernel = _dl.lib().dtb_last_kernel().decode() or None
     if world > 1:
         import torch.distributed as dist
         on_dev = os.environ.get("DTB_BENCH_BACKEND", "nccl") == "nccl"
@@ -448,8 +581,9 @@ def run_e2e(a, w, world, rank, local, dev, barrier):
     px = w["px_rank"] * world
     return {"value": round(px / (ms / 1e3) / 1e6, 1), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
-            "ms_per_step": round(ms, 4), "steps": steps,
-            "path": "paper_1210_3165_b200.binarize / engine C-ABI calls, pinned host buffers"}
+            "ms_per_step": round(ms, 4), "steps": steps, "kernel": e2e_kernel,
+            "path": "paper_1210_3165_b200.binarize / engine C-ABI calls, pinned host buffers "
+                    "(H2D, compute and D2H overlapped in row chunks; each chunk is a band launch)"}
 
 
 # ----------------------------------------------------------------------------- CPU arm
@@ -473,6 +607,10 @@ def cpu_sample(w):
 
 
 def cpu_baseline(w, seconds, reps=None):
+    """The C restatement of the reference's integral engine on all host threads over a bounded
+    sample of the workload, plus the same on one thread and the numpy restatement of the
+    reference's own numpy code (oracle/numpy_ref.py, single-threaded as numpy is) on a
+    512-row slice -- BASELINE.md section 3."""
     import oracle
     threads = len(os.sched_getaffinity(0))
     sub, n, off, desc = cpu_sample(w)
@@ -486,9 +624,35 @@ def cpu_baseline(w, seconds, reps=None):
         if (reps and len(times) >= reps) or (not reps and time.perf_counter() > t_end):
             break
     med = statistics.median(times)
+    one = single_thread_rates(sub, w, min(n, 512))
+    total = w["px_rank"]
     return {"value": round(px / med / 1e6, 2), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{desc}: {px} px, {len(times)} reps, median {med * 1e3:.1f} ms; "
-                      "C restatement of the reference integral engine (oracle/oracle.c)"}
+            "cpu_model": cpu_model(), "sample_fraction": round(px / total, 6),
+            "single_thread": one,
+            "sample": f"{desc}: {px} px ({px / total:.4f} of the rank's pixels; the value is that "
+                      f"sample's rate), {len(times)} reps, median {med * 1e3:.1f} ms; C restatement "
+                      "of the reference integral engine (oracle/oracle.c)"}
+
+
+def single_thread_rates(sub, w, rows):
+    """Mpixel/s on ONE host thread over the first `rows` output rows of the sample: the C port
+    and the numpy restatement of the reference's integral engine."""
+    import numpy as np
+
+    import oracle
+    from oracle import numpy_ref
+    r = w["win"] // 2
+    sl = np.ascontiguousarray(sub[:min(sub.shape[0], rows + 2 * r)])
+    px = sl.shape[0] * sl.shape[1]
+    t = time.perf_counter()
+    oracle.binarize(sl, w["win"], w["method"], w["k"], w["r"], tmap=False, threads=1)
+    c1 = time.perf_counter() - t
+    t = time.perf_counter()
+    numpy_ref.binarize(sl, w["win"], w["method"], w["k"], w["r"])
+    n1 = time.perf_counter() - t
+    return {"c_port_mpix_s": round(px / c1 / 1e6, 2),
+            "numpy_restatement_mpix_s": round(px / n1 / 1e6, 3),
+            "sample_px": int(px)}
 
 
 def run_reference(a):
@@ -508,21 +672,53 @@ def run_reference(a):
         oracle.binarize(sub, w["win"], w["method"], w["k"], w["r"], tmap=False, threads=threads)
     dt = (time.perf_counter() - t0) / a.steps
     v = round(px / dt / 1e6, 2)
+    total = w["px_rank"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(dt * 1e3, 3),
             "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
-            "dtype": "u8 in/out; int64 sums; f64 epilogue", "data": "synthetic",
-            "config": {"workload": w["desc"], "window": w["win"], "parallelism": f"cpu{threads}"},
+            "dtype": "u8 in/out; int64 sums; fp64 epilogue (reference op order)",
+            "data": "synthetic (seeded, paper_1210_3165_b200/workloads.py)",
+            # the GPU arm's workload and parameters; each step times a bounded sample of it
+            "config": {"workload": w["desc"], "image": w["shape"], "window": w["win"],
+                       "method": w["method"], "k": w["k"], "r": w["r"],
+                       "parallelism": f"cpu{threads}", "sample_fraction": round(px / total, 6)},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{desc}: {px} px per step"},
+                             "cpu_model": cpu_model(), "sample_fraction": round(px / total, 6),
+                             "sample": f"{desc}: {px} px per step ({px / total:.4f} of the "
+                                       "workload; value = that sample's rate)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def self_launch(a) -> int:
+    """--gpus N > 1 without torchrun: run this script under torch.distributed.run, N ranks."""
+    import socket
+    if os.environ.get("DTB_BENCH_SAME_DEVICE") != "1":
+        import torch
+        have = torch.cuda.device_count()
+        if have < a.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {a.gpus}: only {have} GPU(s) visible"}))
+            return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+           str(a.gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl == "ours":
+        sys.exit(self_launch(a))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != a.gpus and not (a.impl == "reference" and world == 1):
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":
         run_reference(a)
+    elif a.emulate_bands:
+        run_band_emulation(a)
     else:
         run_ours(a)
 

@@ -1830,9 +1830,16 @@ cudaError_t set_fp32_audit(unsigned long long* counters) {
     return e != cudaSuccess ? e : set_fp32_audit_block(counters);
 }
 
-// DTB_BB: 0 never, 1 whenever eligible, 2 (default) eligible and r >= DTB_BB_MIN_R.
+// DTB_BB: 0 never, 1 whenever eligible, 2 (default): eligible and either r >= DTB_BB_MIN_R, or
+// r >= DTB_BB_MIN_R_LARGE on pages of >= 2^26 output pixels.  Measured (profiles/r02_config_table
+// files): C4 (16384^2, r=63) 0.40 vs 0.50 ms; 4096^2 pages at r=9..49 are 1.2-6x slower on
+// bb_kernel than on the per-pixel kernels (each pipeline's 2r-row warm-up dominates a short
+// band), break even near r=50 and win from r~57 (W115: 0.113 vs 0.117 ms, W243: 0.140 vs 0.154).
 #ifndef DTB_BB_MIN_R
-#define DTB_BB_MIN_R 24
+#define DTB_BB_MIN_R 56
+#endif
+#ifndef DTB_BB_MIN_R_LARGE
+#define DTB_BB_MIN_R_LARGE 24
 #endif
 static int bb_mode() {  // read per launch (tests switch it)
     const char* e = getenv("DTB_BB");
@@ -1888,7 +1895,9 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     };
     {
         const int bbm = bb_mode();
-        if (bbm && bb_eligible(p) && (bbm == 1 || p.r >= DTB_BB_MIN_R))
+        const long long px = (long long)p.cols * (p.out_end - p.out_begin) * n_images;
+        if (bbm && bb_eligible(p) &&
+            (bbm == 1 || p.r >= DTB_BB_MIN_R || (p.r >= DTB_BB_MIN_R_LARGE && px >= (1ll << 26))))
             return launch_block(p, n_images, num_sms, st, print_plan());
     }
     Plan pl = plan_for(V);

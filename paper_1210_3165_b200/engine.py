@@ -1,12 +1,18 @@
 """Device-side entry points: torch tensors as buffers, work done by libdocthresh_b200.
 
 Every function here launches a kernel from libdocthresh_b200.so through the
-C ABI (include/docthresh_b200.h) on the current torch CUDA stream.  Inputs
-may be host numpy arrays (copied to the device) or CUDA uint8 tensors (used in
-place).  There is no CPU path: without a CUDA device these raise.
+C ABI (include/docthresh_b200.h) on the input tensor's device and that device's
+current torch CUDA stream.  Inputs may be host numpy arrays (copied to the
+device) or CUDA uint8 tensors (used in place).  Gray images are handed to the
+kernels with a 16-byte aligned base and row pitch -- the row staging uses bulk
+copies -- so host pages are uploaded into a pitched buffer and a device tensor
+with an odd pitch is first copied into one.  There is no CPU path: without a
+CUDA device these raise.
 """
 
 from __future__ import annotations
+
+import functools
 
 import numpy as np
 
@@ -42,9 +48,38 @@ def is_host_tensor(x) -> bool:
 
 
 def _stream(stream=None) -> int:
+    """The given stream, else the current stream of the current device (the wrapped entry
+    points below make the input's device current)."""
     torch = torch_mod()
     s = torch.cuda.current_stream() if stream is None else stream
     return s.cuda_stream
+
+
+def _on_input_device(fn):
+    """Run fn with the device of its first CUDA tensor argument current, so its launches (and
+    the library's per-device launch state) use that device, not whichever device is current."""
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        for x in list(args) + list(kwargs.values()):
+            if is_device_tensor(x):
+                import torch
+                with torch.cuda.device(x.device):
+                    return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+    return wrapper
+
+
+def _pitched(t):
+    """A 2-D uint8 device image with a 16-byte aligned base and pitch (a view into a pitched
+    copy when t's layout is not)."""
+    if t.dim() == 2 and (t.data_ptr() % 16 or t.stride(0) % 16):
+        torch = torch_mod()
+        h, w = t.shape
+        buf = torch.empty((h, -(-w // 16) * 16), dtype=torch.uint8, device=t.device)
+        v = buf[:, :w]
+        v.copy_(t)
+        return v
+    return t
 
 
 def _check_device_image(t, ndim: int, what: str):
@@ -57,7 +92,7 @@ def _check_device_image(t, ndim: int, what: str):
         raise ValueError("image is empty")
     if t.stride(-1) != 1 or (ndim == 3 and t.stride(1) != 3):
         t = t.contiguous()
-    return t
+    return _pitched(t)
 
 
 def to_device(arr, ndim: int = 2, what: str = "image"):
@@ -65,19 +100,28 @@ def to_device(arr, ndim: int = 2, what: str = "image"):
     torch = torch_mod()
     if is_device_tensor(arr):
         return _check_device_image(arr, ndim, what)
-    if is_host_tensor(arr):
-        return arr.contiguous().to("cuda", non_blocking=True)
-    a = np.ascontiguousarray(arr, dtype=np.uint8)
-    return torch.from_numpy(a).to("cuda")
+    if not is_host_tensor(arr):
+        arr = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint8))
+    arr = arr.contiguous()
+    if ndim == 2 and arr.shape[1] % 16:
+        # upload into a pitched buffer (one 2-D copy): every width reaches the fast kernels
+        h, w = arr.shape
+        buf = torch.empty((h, -(-w // 16) * 16), dtype=torch.uint8, device="cuda")
+        v = buf[:, :w]
+        v.copy_(arr, non_blocking=arr.is_pinned())
+        return v
+    return arr.to("cuda", non_blocking=arr.is_pinned())
 
 
+@_on_input_device
 def binarize(gray, win: int, method: str, k: float, r: float, want_tmap: bool = True,
-             stream=None):
+             stream=None, out=None):
     """Whole-image binarize -> (binary uint8 tensor, tmap float64 tensor or None)."""
     torch = torch_mod()
     g = to_device(gray)
     h, w = g.shape
-    out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
+    if out is None:
+        out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
     tmap = torch.empty((h, w), dtype=torch.float64, device=g.device) if want_tmap else None
     rc = _lib.lib().dtb_binarize(
         g.data_ptr(), g.stride(0), h, w, 0, h, 0, h, out.data_ptr(), out.stride(0),
@@ -100,6 +144,7 @@ def _streams_for(dev):
     return _side_streams[key]
 
 
+@_on_input_device
 def host_streamed(host, band_fn, rad: int, out=None, chunk_rows: int | None = None):
     """Host page -> host binary with H2D, compute and D2H overlapped by row chunks.
 
@@ -117,8 +162,9 @@ def host_streamed(host, band_fn, rad: int, out=None, chunk_rows: int | None = No
     dev = torch.device("cuda", torch.cuda.current_device())
     cur = torch.cuda.current_stream()
     s_in, s_out = _streams_for(dev)
-    dev_in = torch.empty((h, w), dtype=torch.uint8, device=dev)
-    dev_out = torch.empty((h, w), dtype=torch.uint8, device=dev)
+    pitch = -(-w // 16) * 16  # 16-byte pitch: the fast kernels stage rows with bulk copies
+    dev_in = torch.empty((h, pitch), dtype=torch.uint8, device=dev)[:, :w]
+    dev_out = torch.empty((h, pitch), dtype=torch.uint8, device=dev)[:, :w]
     if chunk_rows is None:
         import os
         n = int(os.environ.get("DTB_STREAM_CHUNKS", "16"))
@@ -149,6 +195,7 @@ def host_streamed(host, band_fn, rad: int, out=None, chunk_rows: int | None = No
     return out
 
 
+@_on_input_device
 def binarize_band(buf, row0_global: int, rows_global: int, out_begin: int, out_end: int,
                   win: int, method: str, k: float, r: float, out=None, stream=None):
     """Binarize global rows [out_begin, out_end) from a buffer holding rows [row0, row0+len)."""
@@ -211,6 +258,7 @@ def ipc_close(base: int) -> None:
     _lib.check(_lib.lib().dtb_ipc_close(base), "dtb_ipc_close")
 
 
+@_on_input_device
 def binarize_batch(stack, win: int, method: str, k: float, r: float, out=None, stream=None):
     """(N, H, W) uint8 CUDA stack -> (N, H, W) binary, one launch."""
     torch = torch_mod()
@@ -226,6 +274,7 @@ def binarize_batch(stack, win: int, method: str, k: float, r: float, out=None, s
     return out
 
 
+@_on_input_device
 def window_stats(gray, win: int, want=("mean", "std", "count"), stream=None):
     """dict of requested (rows, cols) device tensors among S, Q, count, mean, std."""
     torch = torch_mod()
@@ -242,6 +291,7 @@ def window_stats(gray, win: int, want=("mean", "std", "count"), stream=None):
     return outs
 
 
+@_on_input_device
 def sampled(gray, offsets, method: str | None = None, k: float = 0.0, r: float = 128.0,
             want_tmap: bool = True, stream=None):
     """Mask-restricted statistics (stats.py:133-163) or binarization with them.
@@ -276,6 +326,7 @@ def sampled(gray, offsets, method: str | None = None, k: float = 0.0, r: float =
 GS_CODES = {"gs1": 1, "gs2": 2, "gs3": 3, "gs4": 4, "gs5": 5, "gs6": 6}
 
 
+@_on_input_device
 def gs(gray, structure: str, win: int, method: str | None = None, k: float = 0.0,
        r: float = 128.0, want_tmap: bool = True, stream=None):
     """GS-mask statistics / binarization in O(1) per pixel (dtb_gs_stats).
@@ -311,6 +362,7 @@ def gs(gray, structure: str, win: int, method: str | None = None, k: float = 0.0
     return res
 
 
+@_on_input_device
 def gs_band(buf, row0_global: int, rows_global: int, out_begin: int, out_end: int,
             structure: str, win: int, method: str, k: float, r: float, out=None, stream=None):
     """GS-mask binarization of global rows [out_begin, out_end) from a row-band buffer
@@ -334,6 +386,7 @@ def gs_band(buf, row0_global: int, rows_global: int, out_begin: int, out_end: in
     return out
 
 
+@_on_input_device
 def to_gray(rgb, stream=None):
     torch = torch_mod()
     t = to_device(rgb, ndim=3, what="rgb")
@@ -345,6 +398,7 @@ def to_gray(rgb, stream=None):
     return out
 
 
+@_on_input_device
 def rgb_binarize(rgb, win: int, method: str, k: float, r: float, want_gray: bool = False,
                  stream=None):
     torch = torch_mod()
@@ -359,6 +413,7 @@ def rgb_binarize(rgb, win: int, method: str, k: float, r: float, want_gray: bool
     return (out, gray) if want_gray else out
 
 
+@_on_input_device
 def histogram(gray, stream=None):
     """256-bin histogram (uint64) of a gray image, on the device."""
     torch = torch_mod()
@@ -371,6 +426,7 @@ def histogram(gray, stream=None):
     return hist
 
 
+@_on_input_device
 def apply_global(gray, t: int, stream=None):
     torch = torch_mod()
     g = to_device(gray)
@@ -382,6 +438,7 @@ def apply_global(gray, t: int, stream=None):
     return out
 
 
+@_on_input_device
 def otsu(gray, stream=None):
     """Device int32 tensor [1] holding the Otsu T (dtb_otsu); no host synchronisation."""
     torch = torch_mod()
@@ -395,6 +452,7 @@ def otsu(gray, stream=None):
     return t
 
 
+@_on_input_device
 def apply_global_dev(gray, t_dev, want_tmap: bool = False, stream=None):
     """(binary, tmap or None) with T from a device int32 tensor (dtb_apply_global_dev)."""
     torch = torch_mod()
@@ -410,6 +468,7 @@ def apply_global_dev(gray, t_dev, want_tmap: bool = False, stream=None):
     return out, tmap
 
 
+@_on_input_device
 def integral_tables(gray, stream=None):
     """(H+1, W+1) int64 summed-area tables of f and f^2 (stats.py:82-91)."""
     torch = torch_mod()

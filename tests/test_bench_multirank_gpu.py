@@ -45,3 +45,37 @@ def test_bench_two_ranks_p2p(cfg):
 def test_bench_reference_arm_two_ranks():
     d = _torchrun(["--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "3"], {})
     assert d["impl"] == "reference" and d["value"] > 0
+
+
+def test_bench_self_launches_n_ranks():
+    # `bench.py --gpus 2` without torchrun re-launches itself under torch.distributed.run
+    env = dict(os.environ, DTB_BENCH_SAME_DEVICE="1", DTB_BENCH_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "c1",
+           "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["halo_bytes_per_step"] == 2 * 7 * 512  # 2 boundaries' worth, r = 7
+
+
+def test_bench_world_mismatch_is_an_error():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--config", "c1", "--steps", "1", "--warmup", "1"], capture_output=True,
+                         text=True, timeout=300, cwd=ROOT, env=env)
+    assert res.returncode != 0 and "WORLD_SIZE" in (res.stdout + res.stderr)
+
+
+def test_band_emulation_mode():
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c5",
+                          "--window", "131", "--emulate-bands", "4", "--steps", "3",
+                          "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-3000:]
+    d = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["mode"] == "band_emulation" and d["band_equals_page_rows"]
+    assert d["ms_per_band"] > 0 and d["halo_bytes_per_band"] == 2 * 65 * 4096
