@@ -469,12 +469,14 @@ int dtb_binarize(const uint8_t* gray, int64_t pitch, int32_t in_rows, int32_t co
         return fail(DTB_E_INVALID,
                     "rows: band needs global rows [%d,%d) but buffer holds [%d,%d)", need0,
                     need1, row0_global, row0_global + in_rows);
-    if (!tmap && slide_ok(rad, cols, rows_global, gray, pitch, 0)) {
+    if (slide_ok(rad, cols, rows_global, gray, pitch, 0) &&
+        (!tmap || (((uintptr_t)tmap | (uintptr_t)tmap_pitch) & 15) == 0)) {
         SlideParams q{};
         q.in = gray; q.pitch = pitch; q.cols = cols; q.row0 = row0_global; q.H = rows_global;
         q.out_begin = out_row_begin; q.out_end = out_row_end; q.r = rad;
         q.rx = std::min(rad, cols - 1);
         q.bin = binary; q.bin_pitch = binary_pitch; q.method = method; q.k = k; q.rr = r;
+        q.tmap = tmap; q.tmap_pitch = tmap_pitch;  // tmap rows = output rows [out_begin, out_end)
         if (out_row_end <= out_row_begin) return DTB_OK;
         const cudaError_t e = launch_slide(q, 1, num_sms(), (cudaStream_t)stream);
         return e == cudaSuccess ? DTB_OK : cuda_fail(e, "slide_kernel launch");

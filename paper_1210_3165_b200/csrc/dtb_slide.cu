@@ -222,6 +222,77 @@ __device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t*
 
 
 
+// TMAP variant of row_outputs: every pixel runs the reference fp64 epilogue (t_exact_fast,
+// bit-exact), its threshold goes to the fp64 map row trow[0..V) and its byte to ow.
+template <int V, int RXM4, bool BORDER>
+__device__ __forceinline__ void row_outputs_tmap(const uint32_t* sPS, const uint32_t* sPQ,
+                                                 const int (&aw)[V / 4 + 1], const int (&bw)[V / 4 + 1],
+                                                 const uint8_t* fsm, uint32_t (&ow)[V / 4], double* trow,
+                                                 int xo, int cols, int ny, int r, const SlideParams& p,
+                                                 double rnN, double rinv) {
+    constexpr int MA = (4 - RXM4) & 3;
+    constexpr int MB = (RXM4 + 1) & 3;
+    uint32_t fw[V / 4];
+#pragma unroll
+    for (int q = 0; q < V / 16; ++q) {
+        const uint4 v = *reinterpret_cast<const uint4*>(fsm + 16 * q);
+        fw[4 * q] = v.x; fw[4 * q + 1] = v.y; fw[4 * q + 2] = v.z; fw[4 * q + 3] = v.w;
+    }
+    const bool full = xo + V <= cols;
+#pragma unroll
+    for (int g = 0; g < V / 8; ++g) {
+        uint32_t S8[8], Q8[8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t* sp = h ? sPQ : sPS;
+            uint32_t A[12], B[12];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (q < 2 || MA) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(sp + aw[2 * g + q]);
+                    A[4 * q] = v.x; A[4 * q + 1] = v.y; A[4 * q + 2] = v.z; A[4 * q + 3] = v.w;
+                }
+                if (q < 2 || MB) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(sp + bw[2 * g + q]);
+                    B[4 * q] = v.x; B[4 * q + 1] = v.y; B[4 * q + 2] = v.z; B[4 * q + 3] = v.w;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t v = B[MB + j] - A[MA + j];
+                if (h) Q8[j] = v; else S8[j] = v;
+            }
+        }
+        uint32_t bytes[2] = {0u, 0u};
+        double t8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t f = __byte_perm(fw[2 * g + (j >> 2)], 0u, 0x4440 | (j & 3));
+            uint32_t n = p.N;
+            double rn = rnN;
+            if (BORDER) {
+                const int x = xo + 8 * g + j;
+                n = (uint32_t)(ny * (min(x + r, cols - 1) - max(x - r, 0) + 1));
+                if (n != p.N) rn = __drcp_rn((double)n);
+            }
+            const double t = t_exact_fast(S8[j], Q8[j], n, rn, p.method, p.k, p.rr, rinv);
+            t8[j] = t;
+            if (!((double)f < t)) bytes[j >> 2] |= 0xFFu << (8 * (j & 3));
+        }
+        ow[2 * g] = bytes[0];
+        ow[2 * g + 1] = bytes[1];
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 8; j += 2)
+                __stcs(reinterpret_cast<double2*>(trow + 8 * g + j), make_double2(t8[j], t8[j + 1]));
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (xo + 8 * g + j < cols) trow[8 * g + j] = t8[j];
+        }
+    }
+}
+
 // register budget: V=16 fits 128 registers without spills (4 CTAs x 4 warps per SM)
 #ifndef DTB_SLIDE_MINB
 #define DTB_SLIDE_MINB(V) ((V) == 16 ? 2 : 1)
@@ -232,6 +303,7 @@ template <int V, int RXM4, int MX>
 __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlideParams p) {
     constexpr int METHOD = MX & 3;
     constexpr bool SEG = (MX & 4) != 0;
+    constexpr bool TMAP = (MX & 8) != 0;  // also write the fp64 threshold map (exact per pixel)
     constexpr int MA = (4 - RXM4) & 3;
     constexpr int MB = (RXM4 + 1) & 3;
     constexpr int NS = SLIDE_STAGES;
@@ -383,6 +455,13 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     // a warp with any x-border thread runs the (per-pixel count) border variant uniformly
     const bool x_border_warp = __any_sync(__activemask(), has_out && !x_interior);
     uint8_t* obase = p.bin + (int64_t)blockIdx.z * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
+    // TMAP: RN(1/N) for the interior count, and 1/R when R is a power of two (exact scaling)
+    double rnN = 0.0, rinv = 0.0;
+    if constexpr (TMAP) {
+        rnN = __drcp_rn((double)p.N);
+        int e;
+        if (frexp(p.rr, &e) == 0.5) rinv = ldexp(1.0, 1 - e);
+    }
 
     auto release = [&](int k) {  // this warp is done with item k's stage
         __syncwarp();
@@ -543,9 +622,18 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
             const int ny = min(y + p.r, p.H - 1) - max(y - p.r, 0) + 1;
             const uint8_t* fsm = stage + 2 * p.NC + V * t;
-            bool unc;
+            bool unc = false;
             uint32_t ow[V / 4];
-            if (y_interior && !x_border_warp)
+            if constexpr (TMAP) {
+                double* trow = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(p.tmap) +
+                                                         (y - p.out_begin) * p.tmap_pitch) + xo;
+                if (y_interior && !x_border_warp)
+                    row_outputs_tmap<V, RXM4, false>(sPS, sPQ, aw, bw, fsm, ow, trow, xo, p.cols, ny,
+                                                     p.r, p, rnN, rinv);
+                else
+                    row_outputs_tmap<V, RXM4, true>(sPS, sPQ, aw, bw, fsm, ow, trow, xo, p.cols, ny,
+                                                    p.r, p, rnN, rinv);
+            } else if (y_interior && !x_border_warp)
                 unc = row_outputs<V, RXM4, METHOD, false>(sPS, sPQ, aw, bw, fsm, ow, xo, p.cols, ny,
                                                           p.r, p);
             else
@@ -1647,6 +1735,11 @@ static cudaError_t dispatch_rx(int m, bool sv, dim3 grid, int nt, size_t smem,
                 if (sv) { DTB_MX(M, DTB_METHOD_SAUVOLA | 4) } else { DTB_MX(M, DTB_METHOD_NIBLACK | 4) } \
             }                                                                                \
         }                                                                                    \
+        if constexpr (V == 16) {                                                             \
+            if (p.tmap) {                                                                    \
+                if (sv) { DTB_MX(M, DTB_METHOD_SAUVOLA | 8) } else { DTB_MX(M, DTB_METHOD_NIBLACK | 8) } \
+            }                                                                                \
+        }                                                                                    \
         if (sv) { DTB_MX(M, DTB_METHOD_SAUVOLA) } else { DTB_MX(M, DTB_METHOD_NIBLACK) }
     switch (m) {
         DTB_CASE(0)
@@ -1874,7 +1967,9 @@ static int slide_band_model() {  // DTB_BAND_MODEL=0: one full wave (the previou
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
     slide_constants(p);
     const int vset = slide_v();
-    int V = p.nseg ? 32 : (vset ? vset : 32);  // segmented variants exist for V = 32 only
+    // segmented variants: V = 32 only; the tmap variant runs V = 16 (half the registers per
+    // thread: twice the resident warps for its fp64 epilogue)
+    int V = p.tmap ? 16 : (p.nseg ? 32 : (vset ? vset : 32));
     const int rows_out = p.out_end - p.out_begin;
     const int alpha = (16 - (p.rx & 15)) & 15;
     // strip plan: w warps -> NC = 32 V w columns; pick the w (1..8) with the least total column
@@ -1896,7 +1991,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     {
         const int bbm = bb_mode();
         const long long px = (long long)p.cols * (p.out_end - p.out_begin) * n_images;
-        if (bbm && bb_eligible(p) &&
+        if (bbm && !p.tmap && bb_eligible(p) &&
             (bbm == 1 || p.r >= DTB_BB_MIN_R || (p.r >= DTB_BB_MIN_R_LARGE && px >= (1ll << 26))))
             return launch_block(p, n_images, num_sms, st, print_plan());
     }
@@ -1984,7 +2079,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // take them when that cuts the staged column work by >= 10% (C2 pages 2480 wide: one strip
     // of 2560 instead of three of 1024 -- W15 0.119 -> 0.058 ms; C5 W3: 0.093 -> 0.078 ms;
     // C5 W67 / W131 within 2%).
-    if (!vset && !p.nseg && V == 32) {
+    if (!vset && !p.nseg && !p.tmap && V == 32) {
         const Plan p16 = plan_for(16);
         if (p16.w > 0 && p16.work * 10 <= pl.work * 9) {
             V = 16;

@@ -122,7 +122,9 @@ def binarize(gray, win: int, method: str, k: float, r: float, want_tmap: bool = 
     h, w = g.shape
     if out is None:
         out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
-    tmap = torch.empty((h, w), dtype=torch.float64, device=g.device) if want_tmap else None
+    # a 16-byte row pitch lets the fast kernel's paired fp64 stores take the map
+    tmap = (torch.empty((h, w + (w & 1)), dtype=torch.float64, device=g.device)[:, :w]
+            if want_tmap else None)
     rc = _lib.lib().dtb_binarize(
         g.data_ptr(), g.stride(0), h, w, 0, h, 0, h, out.data_ptr(), out.stride(0),
         tmap.data_ptr() if tmap is not None else None, (tmap.stride(0) * 8) if tmap is not None else 0,
