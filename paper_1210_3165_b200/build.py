@@ -9,7 +9,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libdocthresh_b200.so")
+# DTB_LIB_OUT: build a variant (e.g. the DTB_DEBUG_BOUNDS / DTB_PERTURB safety build) elsewhere;
+# _lib.py loads it when DTB_LIB_PATH points at it
+LIB = os.environ.get("DTB_LIB_OUT") or os.path.join(HERE, "libdocthresh_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("DTB_NVCC_EXTRA", "").split()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -63,6 +63,27 @@ namespace dtb {
 #endif
 
 
+// DTB_PERTURB=1 (safety builds, scripts/safety_checks.sh): pseudo-random per-lane sleeps at the
+// points where lanes hand data to each other (ring slots, the prefix planes, the exact path's
+// shuffles) and before every bulk-copy issue, so a missing __syncwarp / mbarrier wait shows up
+// as a parity failure.  The pool's compute-sanitizer is closed; this and DTB_DEBUG_BOUNDS are
+// the race / bounds evidence for this kernel.
+#ifndef DTB_PERTURB
+#define DTB_PERTURB 0
+#endif
+#if DTB_PERTURB
+__device__ __forceinline__ void bb_perturb(uint32_t a, uint32_t b) {
+    uint32_t h = (a * 0x9E3779B1u) ^ (b * 0x85EBCA77u) ^ (threadIdx.x * 0xC2B2AE3Du);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if ((h & 7u) == 0) __nanosleep(64 + (h >> 20));  // up to ~4 us on one draw in eight
+}
+#define BB_PERTURB(a, b) bb_perturb((uint32_t)(a), (uint32_t)(b))
+#else
+#define BB_PERTURB(a, b) ((void)0)
+#endif
+
 // words of one prefix plane: entries P[2m] (even) or P[2m+1] (odd), m <= NB/2, 16-byte padded
 __host__ __device__ constexpr int bb_plane_words(int NB) { return ((NB / 2 + 1) + 3) & ~3; }
 
@@ -371,6 +392,7 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
     // one issue site: iteration k first refills the slot item k-1 left (item k+NS-1), then
     // consumes item k; the first NS-1 iterations only fill the ring
     for (int k = 1 - NS; k < n_items; ++k) {
+        BB_PERTURB(pid, 4 * k);
         if (k + NS - 1 < n_items) do {
             const int kk = k + NS - 1;
             const int s = kk % NS;
@@ -409,6 +431,7 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
         if (k < 0) continue;
         const int s = k % NS;
         mbar_wait(&full[s], (k / NS) & 1);
+        BB_PERTURB(pid, 4 * k + 1);
         const uint8_t* stage = ring + s * 3 * NC;
         if (k < nwarm) {
             const int cnt = min(3, nwr - 3 * k);
@@ -457,6 +480,7 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
                     const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
                     if (lane >= off) { iS += vs; iQ += vq; }
                 }
+                BB_PERTURB(pid, 4 * k + 2);
                 // lane's exclusive prefix P[16 lane + j]: even j -> even plane, odd j -> odd plane
                 uint32_t vS = iS - TS, vQ = iQ - TQ;
 #pragma unroll
@@ -481,6 +505,7 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
                 }
             }
             __syncwarp();
+            BB_PERTURB(pid, 4 * k + 3);
             // ---- output side: groups of 8 pixels
             const uint8_t* F = stage + 2 * NC;
             const int ny = min(y + r, p.H - 1) - max(y - r, 0) + 1;

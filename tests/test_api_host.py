@@ -101,3 +101,21 @@ def test_pnm_codec_round_trip(rng):
         dt.read_pnm(b"P5 2 2 255 " + bytes([1, 2, 3]))
     with pytest.raises(dt.PnmError, match="maxval"):
         dt.read_pnm(b"P5 1 1 65535 " + bytes([0, 0]))
+
+
+def test_gen_synthetic_matches_reference_pages():
+    # tests/golden/metrics.npz holds pages made by the reference's own gen_synthetic
+    import numpy as np
+    from conftest import GOLDEN
+    import os
+    from paper_1210_3165_b200 import SyntheticSpec, gen_synthetic, memory_model
+    z = np.load(os.path.join(GOLDEN, "metrics.npz"))
+    specs = [SyntheticSpec(), SyntheticSpec(width=300, height=180, noise_seed=3, noise_amplitude=20)]
+    for i, sp in enumerate(specs):
+        img, gt = gen_synthetic(sp)
+        assert np.array_equal(img, z[f"page{i}"]) and np.array_equal(gt, z[f"page_gt{i}"])
+    assert memory_model("integral", 10) == 120
+    with pytest.raises(ValueError, match="engine"):
+        memory_model("fast", 10)
+    with pytest.raises(ValueError, match="too small"):
+        gen_synthetic(SyntheticSpec(width=8))
