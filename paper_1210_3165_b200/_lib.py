@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdocthresh_b200.so")
+LIB_PATH = os.environ.get("DTB_LIB_PATH") or os.path.join(HERE, "libdocthresh_b200.so")  # safety builds
 
 DTB_METHOD_NIBLACK = 1
 DTB_METHOD_SAUVOLA = 2

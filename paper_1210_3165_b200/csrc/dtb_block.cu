@@ -645,14 +645,9 @@ bool bb_eligible(const SlideParams& p) {
 
 struct BBCache {
     std::mutex mu;
-    int occ[64][2][2];          // [device][seg][variant] CTAs (= pipelines) per SM (0 = unknown)
-    bool smem_set[64][2][2];    // dynamic-smem opt-in raised
+    int occ[64][2];          // [device][seg] CTAs (= pipelines) per SM (0 = unknown)
+    bool smem_set[64][2];    // dynamic-smem opt-in raised
 };
-// register-budget variants: 128 registers (16 pipelines per SM) or 168 (12 per SM)
-static int bb_variant() {
-    const char* e = getenv("DTB_BB_MINB");
-    return (e && atoi(e) == 12) ? 1 : 0;
-}
 static BBCache g_bb;
 
 template <bool SEG, int MINB>
@@ -660,14 +655,13 @@ static cudaError_t bb_prepare(int dev, int* occ) {
     std::lock_guard<std::mutex> lk(g_bb.mu);
     if (dev < 0 || dev >= 64) return cudaErrorInvalidValue;
     auto fn = bb_kernel<SEG, MINB>;
-    const int v = MINB == 16 ? 0 : 1;
     const size_t smem = BB_WARP_BYTES;
-    if (!g_bb.smem_set[dev][SEG][v]) {
+    if (!g_bb.smem_set[dev][SEG]) {
         const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        g_bb.smem_set[dev][SEG][v] = true;
+        g_bb.smem_set[dev][SEG] = true;
     }
-    int& o = g_bb.occ[dev][SEG][v];
+    int& o = g_bb.occ[dev][SEG];
     if (!o) {
         const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32, smem);
         if (e != cudaSuccess) return e;
@@ -719,13 +713,10 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     int occ = 1;
-    const int var = bb_variant();
-    e = var ? (p.nseg ? bb_prepare<true, 12>(dev, &occ) : bb_prepare<false, 12>(dev, &occ))
-            : (p.nseg ? bb_prepare<true, 16>(dev, &occ) : bb_prepare<false, 16>(dev, &occ));
+    e = p.nseg ? bb_prepare<true, 16>(dev, &occ) : bb_prepare<false, 16>(dev, &occ);
     if (e != cudaSuccess) return e;
     const int rows_out = p.out_end - p.out_begin;
-    int nbands = bb_plan_bands(rows_out, ns * n_images, num_sms * occ, p.r);
-    if (const char* e = getenv("DTB_BB_BANDS")) nbands = std::max(1, std::min(atoi(e), rows_out));  // A/B
+    const int nbands = bb_plan_bands(rows_out, ns * n_images, num_sms * occ, p.r);
     p.TH = (rows_out + nbands - 1) / nbands;
     const int nb = (rows_out + p.TH - 1) / p.TH;
     const long long np = (long long)ns * nb * n_images;
@@ -736,13 +727,8 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
         fprintf(stderr, "[dtb plan] bb_kernel cols=%d rows=%d r=%d strips=%d TW=%d (first %d) bands=%d TH=%d pipes=%lld ctas=%d occ=%d smem=%zu\n",
                 p.cols, rows_out, p.r, ns, p.TW, tw0, nb, p.TH, np, ctas, occ, smem);
     set_last_kernel("bb_kernel");
-    if (var) {
-        if (p.nseg) bb_kernel<true, 12><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
-        else bb_kernel<false, 12><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
-    } else {
-        if (p.nseg) bb_kernel<true, 16><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
-        else bb_kernel<false, 16><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
-    }
+    if (p.nseg) bb_kernel<true, 16><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
+    else bb_kernel<false, 16><<<ctas, 32, smem, st>>>(p, ns, nb, tw0);
     return cudaGetLastError();
 }
 

@@ -401,7 +401,6 @@ static int launch_strip(StripParams p, int n_images, cudaStream_t st) {
 // (<= 8 warps = 8192 columns) must hold a window plus 32 outputs.
 bool slide_ok(int r, int cols, int rows, const void* base, int64_t pitch,
                      int64_t stride) {
-    if (const char* env = getenv("DTB_FORCE_V1")) { if (env[0] == '1') return false; }
     // rows are staged with 16-byte bulk copies
     if (((uintptr_t)base | (uintptr_t)pitch | (uintptr_t)stride) & 15) return false;
     const double rx = std::min(r, cols - 1), ry = std::min(r, rows - 1);

@@ -32,33 +32,19 @@
 
 #include <algorithm>
 #include <cmath>
-#include <cstdlib>
 #include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "docthresh_b200.h"
 #include "dtb_common.cuh"
 #include "dtb_slide.cuh"
 #include "dtb_async.cuh"
 
-// Tuning switches (measured on B200, C4: quarters 0.662 vs 0.684 ms; a 3-lane producer 0.73 ms)
-#ifndef DTB_PREFIX_QUARTERS
-#define DTB_PREFIX_QUARTERS 1
-#endif
 #ifndef DTB_WS_DEFAULT
 #define DTB_WS_DEFAULT 2  // 0 classic, 1 always warp-specialized, 2 auto
-#endif
-#ifndef DTB_ALU_BALANCE
-#define DTB_ALU_BALANCE 0
-#endif
-// diagnostics only (wrong results): 1 = skip the output phase, 2 = skip prefix stores
-#ifndef DTB_DIAG_SKIP
-#define DTB_DIAG_SKIP 0
-#endif
-#ifndef DTB_D_SPLIT
-#define DTB_D_SPLIT 0
-#endif
-#ifndef DTB_PAR_PRODUCER
-#define DTB_PAR_PRODUCER 0
 #endif
 
 namespace dtb {
@@ -334,7 +320,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     const int f_hi = min(X0 + p.TW, p.cols);
     const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
 
-    // warm-up items carry up to 3 warm-up rows each (E, O, F slots), as in gb_kernel
+    // warm-up items carry up to 3 warm-up rows each (E, O, F slots)
     Items it;
     it.g0 = max(ya - p.r, 0);
     const int nwr = min(ya + p.r, p.H - 1) - it.g0 + 1;  // warm-up rows
@@ -361,77 +347,47 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     // treat them as zero.  The byte tail beyond the last 16-byte chunk is written by thread 0
     // with generic stores (visible to consumers after the barriers in between).
     const uint64_t pol_keep = make_policy(p.l2hint ? 2 : 0), pol_drop = make_policy(p.l2hint ? 1 : 0);
-    // Lanes 0..2 of warp 0 issue the entering / leaving / centre copies in parallel; lane 0 also
-    // arms the full barrier with the byte count (tx-count may transiently go negative).
-    auto issue = [&](int k, int which) {
+    // The byte tail of a ragged row is written with generic stores BEFORE the arrive that arms
+    // the stage: the arrive (release) publishes them to the consumers that wait on the stage.
+    auto issue = [&](int k) {
         const int s = k % NS;
         if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
         uint8_t* E = ring + (size_t)s * 3 * p.NC;
         uint8_t* O = E + p.NC;
         uint8_t* F = O + p.NC;
-        int ge, go = -1, gf = -1;
+        const uint32_t rowb = (uint32_t)(c_hi16 - c_lo);
         if (k < it.nwarm) {
             // warm-up rows g0+3k .. g0+3k+2 into the E, O, F slots (full strip width each)
-            if ((!DTB_PAR_PRODUCER || which == 0)) {
-                const uint32_t rowb = (uint32_t)(c_hi16 - c_lo);
-                const int g = it.g0 + 3 * k, cnt = min(3, it.g0 + nwr - g);
-                mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
-                for (int i = 0; i < cnt; ++i) {
-                    uint8_t* D = E + i * p.NC;
-                    if (rowb) bulk_g2s(D + (c_lo - xc0), row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
-                    for (int c = c_hi16; c < c_hi; ++c) D[c - xc0] = row_at<SEG>(p, in0, g + i)[c];
-                }
-            }
+            const int g = it.g0 + 3 * k, cnt = min(3, it.g0 + nwr - g);
+            for (int i = 0; i < cnt; ++i)
+                for (int c = c_hi16; c < c_hi; ++c) E[i * p.NC + c - xc0] = row_at<SEG>(p, in0, g + i)[c];
+            mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
+            for (int i = 0; i < cnt; ++i)
+                if (rowb) bulk_g2s(E + i * p.NC + (c_lo - xc0), row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
             return;
-        } else {
-            const int y = it.ya + (k - it.nwarm);
-            gf = y;
-            ge = (k == it.nwarm) ? -1 : y + p.r;
-            go = (k == it.nwarm) ? -1 : y - p.r - 1;
-            if (ge >= p.H) ge = -1;
         }
-        const uint32_t rowb = (uint32_t)(c_hi16 - c_lo), fb = (uint32_t)(f_hi16 - X0);
-        if (!DTB_PAR_PRODUCER) {
-            uint32_t bytes = 0;
-            if (ge >= 0) bytes += rowb;
-            if (go >= 0) bytes += rowb;
-            if (gf >= 0) bytes += fb;
-            mbar_expect_tx(&full[s], bytes);
-            if (ge >= 0 && rowb)
-                bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
-            if (go >= 0 && rowb)
-                bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
-            if (gf >= 0 && fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
-            for (int c = c_hi16; c < c_hi; ++c) {
-                if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
-                if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
-            }
-            for (int c = f_hi16; c < f_hi; ++c)
-                if (gf >= 0) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
-        } else if (which == 0) {
-            uint32_t bytes = 0;
-            if (ge >= 0) bytes += rowb;
-            if (go >= 0) bytes += rowb;
-            if (gf >= 0) bytes += fb;
-            mbar_expect_tx(&full[s], bytes);
-            if (ge >= 0 && rowb)
-                bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
-            for (int c = c_hi16; c < c_hi; ++c) {
-                if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
-                if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
-            }
-            for (int c = f_hi16; c < f_hi; ++c)
-                if (gf >= 0) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
-        } else if (which == 1) {
-            if (go >= 0 && rowb)
-                bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
-        } else {
-            if (gf >= 0 && fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
+        const int y = it.ya + (k - it.nwarm);
+        const int gf = y;
+        int ge = (k == it.nwarm) ? -1 : y + p.r;
+        const int go = (k == it.nwarm) ? -1 : y - p.r - 1;
+        if (ge >= p.H) ge = -1;
+        const uint32_t fb = (uint32_t)(f_hi16 - X0);
+        for (int c = c_hi16; c < c_hi; ++c) {
+            if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
+            if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
         }
+        for (int c = f_hi16; c < f_hi; ++c) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
+        uint32_t bytes = fb;
+        if (ge >= 0) bytes += rowb;
+        if (go >= 0) bytes += rowb;
+        mbar_expect_tx(&full[s], bytes);
+        if (ge >= 0 && rowb) bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
+        if (go >= 0 && rowb) bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+        if (fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
     };
-    const bool producer = DTB_PAR_PRODUCER ? (warp == 0 && lane < 3) : (t == 0);
+    const bool producer = (t == 0);
     if (producer)
-        for (int k = 0; k < min(NS - 1, it.n); ++k) issue(k, lane);
+        for (int k = 0; k < min(NS - 1, it.n); ++k) issue(k);
 
     uint32_t cS[V], cQ[V];
 #pragma unroll
@@ -489,7 +445,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             }
         }
         release(k);
-        if (producer && k + NS - 1 < it.n) issue(k + NS - 1, lane);
+        if (producer && k + NS - 1 < it.n) issue(k + NS - 1);
     }
 #pragma unroll
     for (int j = 0; j < V; ++j) { qS[j / (V / 4)] += cS[j]; qQ[j / (V / 4)] += cQ[j]; }
@@ -535,23 +491,15 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
-#if DTB_ALU_BALANCE
-            cS[j] = cS[j] + ev - ov;                 // IADD3 (ALU pipe)
-            const uint32_t nov = 0u - ov;            // IADD3
-            cQ[j] = ev * ev + cQ[j];                 // IMAD
-            cQ[j] = nov * ov + cQ[j];                // IMAD
-#else
             const uint32_t dv = ev - ov;
             cS[j] += dv;
             cQ[j] += dv * (ev + ov);
-#endif
         }
         if (lane == 31) { sWS[warp] = iS; sWQ[warp] = iQ; }
         __syncthreads();
-        if (producer && k + NS - 1 < it.n) issue(k + NS - 1, lane);
+        if (producer && k + NS - 1 < it.n) issue(k + NS - 1);
         uint32_t bS = iS - TS, bQ = iQ - TQ;
         for (int w = 0; w < warp; ++w) { bS += sWS[w]; bQ += sWQ[w]; }
-#if DTB_PREFIX_QUARTERS
         // logical word Vt + m holds P[Vt + m - 1]: the first slot is this thread's base.
         // Four independent running chains, one per quarter of the thread's columns.
         uint32_t cbS[4], cbQ[4];
@@ -566,14 +514,6 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             for (int h = 0; h < 4; ++h) {
                 const int c0 = h * (V / 4) + j;
                 uint4 vs, vq;
-#if DTB_ALU_BALANCE
-                // P[j+1] = P[j-1] + c[j] + c[j+1]: 3-input adds (IADD3) halve the chain depth
-                vs.x = cbS[h]; vq.x = cbQ[h];
-                vs.y = cbS[h] + cS[c0]; vq.y = cbQ[h] + cQ[c0];
-                vs.z = cbS[h] + cS[c0] + cS[c0 + 1]; vq.z = cbQ[h] + cQ[c0] + cQ[c0 + 1];
-                vs.w = vs.y + cS[c0 + 1] + cS[c0 + 2]; vq.w = vq.y + cQ[c0 + 1] + cQ[c0 + 2];
-                cbS[h] = vs.z + cS[c0 + 2] + cS[c0 + 3]; cbQ[h] = vq.z + cQ[c0 + 2] + cQ[c0 + 3];
-#else
                 vs.x = cbS[h]; vq.x = cbQ[h];
                 cbS[h] += cS[c0]; cbQ[h] += cQ[c0];
                 vs.y = cbS[h]; vq.y = cbQ[h];
@@ -582,33 +522,12 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
                 cbS[h] += cS[c0 + 2]; cbQ[h] += cQ[c0 + 2];
                 vs.w = cbS[h]; vq.w = cbQ[h];
                 cbS[h] += cS[c0 + 3]; cbQ[h] += cQ[c0 + 3];
-#endif
                 const int pw = pchunk_word((V / 4) * t + c0 / 4);
                 DTB_CHECK(pw >= 0 && pw + 4 <= NCp);
-                if (!(DTB_DIAG_SKIP & 2)) {
-                    *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
-                    *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
-                }
+                *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
+                *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
             }
         }
-#else
-        // logical word Vt + m holds P[Vt + m - 1]: the first slot is this thread's base
-#pragma unroll
-        for (int j = 0; j < V; j += 4) {
-            uint4 vs, vq;
-            vs.x = bS; vq.x = bQ;
-            bS += cS[j]; bQ += cQ[j];
-            vs.y = bS; vq.y = bQ;
-            bS += cS[j + 1]; bQ += cQ[j + 1];
-            vs.z = bS; vq.z = bQ;
-            bS += cS[j + 2]; bQ += cQ[j + 2];
-            vs.w = bS; vq.w = bQ;
-            bS += cS[j + 3]; bQ += cQ[j + 3];
-            const int pw = pchunk_word((V / 4) * t + j / 4);
-            *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
-            *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
-        }
-#endif
         if (t == blockDim.x - 1) {  // logical word NC = P[NC - 1]
             const int pw = pchunk_word(p.NC / 4);
             sPS[pw] = bS;
@@ -617,7 +536,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
         __syncthreads();
 
         // ---- outputs
-        if (has_out && !(DTB_DIAG_SKIP & 1)) {
+        if (has_out) {
             const bool y_interior = (y - p.r >= 0) && (y + p.r <= p.H - 1);
             uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
             const int ny = min(y + p.r, p.H - 1) - max(y - p.r, 0) + 1;
@@ -671,28 +590,9 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
 // =====================================================================================
 
 
-#ifndef DTB_WS_V16_DEFAULT
-#define DTB_WS_V16_DEFAULT 0  // C4: 0.759 ms with V = VO = 16 (24 warps/SM) vs 0.609 with 32 (12)
-#endif
 
-#ifndef DTB_WS_UNIFORM_OFFS
-#define DTB_WS_UNIFORM_OFFS 0  // C4: 0.6165 (1) vs 0.6086 (0) ms -- the compiler keeps them per-thread anyway
-#endif
 
-#ifndef DTB_WS_ISSUE_POS
-#define DTB_WS_ISSUE_POS 2  // C4: 0.6122 (2) vs 0.6153 (0) vs 0.674 (1) ms at 4 stages
-#endif
 
-#ifndef DTB_WS_SWAP_BUILD
-#define DTB_WS_SWAP_BUILD 0
-#endif
-
-// Warm-up split: the 2r+1 rows that prime a band's column sums are consumed alternately by
-// the column warps (even items) and the otherwise idle output warps (odd items, partial sums
-// for the same columns), which hand their partials over through the not-yet-used prefix area.
-#ifndef DTB_WS_SPLIT_WARM
-#define DTB_WS_SPLIT_WARM 0  // measured no gain on C4 (0.6157 vs 0.6149 ms); kept for A/B
-#endif
 
 #ifndef DTB_WS_MAXREG
 #define DTB_WS_MAXREG 168
@@ -720,19 +620,9 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
     uint8_t* ring = reinterpret_cast<uint8_t*>(empty + NS);
     const int ncw = p.ncw, now = p.now, nthr = 32 * (ncw + now);
 
-    // Logical thread index.  Warp w of a CTA issues from SM sub-partition w % 4, so with
-    // fixed role slots every sub-partition would host one role only (column warps idle at
-    // barriers on two of them while output warps saturate the other two).  Alternate groups
-    // of CTAs (role_div = SMs, i.e. one group per residency wave) put the output role first.
-    const int tp = threadIdx.x;
-#if DTB_WS_SWAP_BUILD
-    const int bid = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
-    const bool swap = p.role_div > 0 && ((bid / p.role_div) & 1);
-    const int t = swap ? (tp < 32 * now ? tp + 32 * ncw : tp - 32 * now) : tp;
-#else
-    const int t = tp;  // role slots fixed (the swap measured slower; build with -DDTB_WS_SWAP_BUILD=1)
-#endif
-    const int lane = tp & 31, warp = t >> 5;
+    // warps [0, ncw) are the column warps, [ncw, ncw + now) the output warps
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
     const bool is_col = warp < ncw;
     const uint8_t* in = p.in + (int64_t)blockIdx.z * p.img_stride;
     const int X0 = (int)blockIdx.x * p.TW;
@@ -747,7 +637,7 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
     const int c_hi16 = c_lo + ((max(c_hi - c_lo, 0)) & ~15);
     const int f_hi = min(X0 + p.TW, p.cols);
     const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
-    // warm-up items carry up to 3 warm-up rows each (E, O, F slots), as in gb_kernel
+    // warm-up items carry up to 3 warm-up rows each (E, O, F slots)
     Items it;
     it.g0 = max(ya - p.r, 0);
     const int nwr = min(ya + p.r, p.H - 1) - it.g0 + 1;  // warm-up rows
@@ -770,50 +660,41 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
     __syncthreads();
 
     const uint64_t pol_keep = make_policy(p.l2hint ? 2 : 0), pol_drop = make_policy(p.l2hint ? 1 : 0);
+    // ragged byte tails first, then the arrive that arms the stage publishes them (release)
     auto issue = [&](int k) {
         const int s = k % NS;
         if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
         uint8_t* E = ring + (size_t)s * 3 * p.NC;
         uint8_t* O = E + p.NC;
         uint8_t* F = O + p.NC;
-        int ge, go = -1, gf = -1;
+        const uint32_t rowb = (uint32_t)(c_hi16 - c_lo);
         if (k < it.nwarm) {
-            // warm-up rows g0+3k .. g0+3k+2 into the E, O, F slots (full strip width each)
-            if (true) {
-                const uint32_t rowb = (uint32_t)(c_hi16 - c_lo);
-                const int g = it.g0 + 3 * k, cnt = min(3, it.g0 + nwr - g);
-                mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
-                for (int i = 0; i < cnt; ++i) {
-                    uint8_t* D = E + i * p.NC;
-                    if (rowb) bulk_g2s(D + (c_lo - xc0), row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
-                    for (int c = c_hi16; c < c_hi; ++c) D[c - xc0] = row_at<SEG>(p, in0, g + i)[c];
-                }
-            }
+            const int g = it.g0 + 3 * k, cnt = min(3, it.g0 + nwr - g);
+            for (int i = 0; i < cnt; ++i)
+                for (int c = c_hi16; c < c_hi; ++c) E[i * p.NC + c - xc0] = row_at<SEG>(p, in0, g + i)[c];
+            mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
+            for (int i = 0; i < cnt; ++i)
+                if (rowb) bulk_g2s(E + i * p.NC + (c_lo - xc0), row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
             return;
-        } else {
-            const int y = it.ya + (k - it.nwarm);
-            gf = y;
-            ge = (k == it.nwarm) ? -1 : y + p.r;
-            go = (k == it.nwarm) ? -1 : y - p.r - 1;
-            if (ge >= p.H) ge = -1;
         }
-        const uint32_t rowb = (uint32_t)(c_hi16 - c_lo), fb = (uint32_t)(f_hi16 - X0);
-        uint32_t bytes = 0;
-        if (ge >= 0) bytes += rowb;
-        if (go >= 0) bytes += rowb;
-        if (gf >= 0) bytes += fb;
-        mbar_expect_tx(&full[s], bytes);
-        if (ge >= 0 && rowb)
-            bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
-        if (go >= 0 && rowb)
-            bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
-        if (gf >= 0 && fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
+        const int y = it.ya + (k - it.nwarm);
+        const int gf = y;
+        int ge = (k == it.nwarm) ? -1 : y + p.r;
+        const int go = (k == it.nwarm) ? -1 : y - p.r - 1;
+        if (ge >= p.H) ge = -1;
+        const uint32_t fb = (uint32_t)(f_hi16 - X0);
         for (int c = c_hi16; c < c_hi; ++c) {
             if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
             if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
         }
-        for (int c = f_hi16; c < f_hi; ++c)
-            if (gf >= 0) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
+        for (int c = f_hi16; c < f_hi; ++c) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
+        uint32_t bytes = fb;
+        if (ge >= 0) bytes += rowb;
+        if (go >= 0) bytes += rowb;
+        mbar_expect_tx(&full[s], bytes);
+        if (ge >= 0 && rowb) bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
+        if (go >= 0 && rowb) bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
+        if (fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
     };
 
     if (is_col) {
@@ -825,12 +706,7 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
 #pragma unroll
         for (int j = 0; j < V; ++j) { cS[j] = 0; cQ[j] = 0; }
         uint32_t qS[4] = {0, 0, 0, 0}, qQ[4] = {0, 0, 0, 0};
-        // warm-up split: column warp c has a helper (output warp c) when c < now; helped warps
-        // take the even items only, unhelped ones every item.  Arrivals per item stay ncw + now.
-        const bool split = DTB_WS_SPLIT_WARM && it.nwarm > 1;
-        const int nh = min(ncw, now);  // helped column warps
-        const bool helped = split && warp < nh;
-        for (int k = 0; k < it.nwarm; k += helped ? 2 : 1) {
+        for (int k = 0; k < it.nwarm; ++k) {
             const int s = k % NS;
             mbar_wait(&full[s], (k / NS) & 1);
             const int cnt = min(3, nwr - 3 * k);
@@ -850,27 +726,11 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
                 }
             }
             __syncwarp();
-            // even items: warp 0 also arrives for the output warps; odd items (unhelped warps
-            // only): the output warps arrive for the helped column warps
-            if (lane == 0)
-                mbar_arrive_cnt(&empty[s], (warp == 0 && (!split || (k & 1) == 0)) ? 1 + now : 1);
+            // warm-up items are read by the column warps only: warp 0 arrives for the output warps
+            if (lane == 0) mbar_arrive_cnt(&empty[s], warp == 0 ? 1 + now : 1);
             if (t == 0)
                 while (issued < min(k + NS, it.n)) issue(issued++);
         }
-#if DTB_WS_SPLIT_WARM
-        if (split) {
-            nbar_sync(BAR_WARM, nthr);  // the helpers' partial sums (odd items) are in smem
-            if (helped) {
-                const uint4* hp = reinterpret_cast<const uint4*>(sm + 2 * V * t);
-#pragma unroll
-                for (int q = 0; q < V / 4; ++q) {
-                    const uint4 a = hp[q], b = hp[V / 4 + q];
-                    cS[4 * q] += a.x; cS[4 * q + 1] += a.y; cS[4 * q + 2] += a.z; cS[4 * q + 3] += a.w;
-                    cQ[4 * q] += b.x; cQ[4 * q + 1] += b.y; cQ[4 * q + 2] += b.z; cQ[4 * q + 3] += b.w;
-                }
-            }
-        }
-#endif
 #pragma unroll
         for (int j = 0; j < V; ++j) { qS[j / (V / 4)] += cS[j]; qQ[j / (V / 4)] += cQ[j]; }
 
@@ -924,14 +784,6 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
             for (int w = 0; w < warp; ++w) { bS += sWS[8 * b + w]; bQ += sWQ[8 * b + w]; }
             // wait until the output warps have consumed row k-2 from this prefix buffer
             nbar_sync(BAR_FREE0 + b, nthr);
-            // Row staging for a later row.  Issuing item j needs item j-NS released by every
-            // warp; FREE(k-2) guarantees that for j <= k+NS-2, so ISSUE_POS 1 never stalls the
-            // producer here, while ISSUE_POS 0 (lookahead NS-1) can hold column warp 0 -- and
-            // with it READY(k) -- until the output warps finish row k-1.
-            if (DTB_WS_ISSUE_POS == 0 && t == 0)
-                while (issued < min(k + NS - 1, it.n)) issue(issued++);
-            if (DTB_WS_ISSUE_POS == 1 && t == 0)
-                while (issued < min(k + NS - 2, it.n)) issue(issued++);
             uint32_t* sPS = sm + (2 * b) * NCp;
             uint32_t* sPQ = sm + (2 * b + 1) * NCp;
             uint32_t cbS[4], cbQ[4];
@@ -964,7 +816,7 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
                 sPQ[pw] = cbQ[3];
             }
             nbar_arrive(BAR_READY0 + b, nthr);
-            if (DTB_WS_ISSUE_POS == 2 && t == 0)  // after publishing row k: off READY's path
+            if (t == 0)  // row staging after publishing row k: off READY's path
                 while (issued < min(k + NS - 1, it.n)) issue(issued++);
         }
         // consume the output warps' last FREE arrivals so no named barrier is left pending
@@ -981,74 +833,13 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
                               ((reinterpret_cast<uintptr_t>(p.bin) | (uintptr_t)p.bin_pitch |
                                 (uintptr_t)p.out_stride) & 15) == 0;
         const bool x_interior = (p.rx == p.r) && (xo - p.r >= 0) && (xo + VO - 1 + p.r <= p.cols - 1);
-#if DTB_WS_UNIFORM_OFFS
-        // Run chunk addresses = per-thread base + launch-uniform offsets: thread `to`'s A run
-        // starts at chunk 8*to + dA (dA = (alpha - MA)/4 in 0..3, the same for every thread),
-        // and pchunk_word(8*to + d) = 36*to + 4*(d + d/8) for d >= 0, so the compiler can keep
-        // the 2 x 9 offsets in uniform registers instead of per-thread ones.
-        static_assert(VO == 32, "uniform run offsets assume 8 chunks per output thread");
-        const int dA = (alpha - MA) >> 2, dB = (alpha + 2 * p.rx + 1 - MB) >> 2;
-        const int tb = 36 * to;
-        int aw[VO / 4 + 1], bw[VO / 4 + 1];
-#pragma unroll
-        for (int i = 0; i < VO / 4 + 1; ++i) {
-            aw[i] = tb + 4 * (dA + i + ((dA + i) >> 3));
-            bw[i] = tb + 4 * (dB + i + ((dB + i) >> 3));
-            DTB_CHECK(aw[i] == pchunk_word(((alpha + VO * to - MA) >> 2) + i));
-            DTB_CHECK(bw[i] == pchunk_word(((alpha + 2 * p.rx + 1 + VO * to - MB) >> 2) + i));
-        }
-#else
         const int la0 = (alpha + VO * to - MA) >> 2;
         const int lb0 = (alpha + 2 * p.rx + 1 + VO * to - MB) >> 2;
         int aw[VO / 4 + 1], bw[VO / 4 + 1];
 #pragma unroll
         for (int i = 0; i < VO / 4 + 1; ++i) { aw[i] = pchunk_word(la0 + i); bw[i] = pchunk_word(lb0 + i); }
-#endif
         const bool x_border_warp = __any_sync(0xffffffffu, has_out && !x_interior);
         uint8_t* obase = p.bin + (int64_t)blockIdx.z * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
-#if DTB_WS_SPLIT_WARM
-        if (it.nwarm > 1) {
-            // odd warm-up items: partial column sums for column thread `to`'s columns
-            const int nh = min(ncw, now);
-            const bool helper = to < 32 * nh;
-            uint32_t hS[V], hQ[V];
-#pragma unroll
-            for (int j = 0; j < V; ++j) { hS[j] = 0; hQ[j] = 0; }
-            for (int k = 1; k < it.nwarm; k += 2) {
-                const int s = k % NS;
-                mbar_wait(&full[s], (k / NS) & 1);
-                if (helper) {
-                    for (int i = 0; i < min(3, nwr - 3 * k); ++i) {
-                        const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * p.NC + i * p.NC + V * to);
-                        uint32_t w[V / 4];
-#pragma unroll
-                        for (int q = 0; q < V / 16; ++q) {
-                            const uint4 a = E[q];
-                            w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
-                        }
-#pragma unroll
-                        for (int j = 0; j < V; ++j) {
-                            const uint32_t v = byte_at(w, j);
-                            hS[j] += v;
-                            hQ[j] += v * v;
-                        }
-                    }
-                }
-                __syncwarp();
-                // output warp 0 arrives for the helped column warps, which skip odd items
-                if (lane == 0) mbar_arrive_cnt(&empty[s], (to >> 5) == 0 ? 1 + nh : 1);
-            }
-            if (helper) {
-                uint4* hp = reinterpret_cast<uint4*>(sm + 2 * V * to);
-#pragma unroll
-                for (int q = 0; q < V / 4; ++q) {
-                    hp[q] = make_uint4(hS[4 * q], hS[4 * q + 1], hS[4 * q + 2], hS[4 * q + 3]);
-                    hp[V / 4 + q] = make_uint4(hQ[4 * q], hQ[4 * q + 1], hQ[4 * q + 2], hQ[4 * q + 3]);
-                }
-            }
-            nbar_arrive(BAR_WARM, nthr);
-        }
-#endif
         nbar_arrive(BAR_FREE0, nthr);  // both prefix buffers start free
         nbar_arrive(BAR_FREE0 + 1, nthr);
         for (int k = it.nwarm; k < it.n; ++k) {
@@ -1097,565 +888,6 @@ __global__ void __maxnreg__(V == 16 ? DTB_WS_MAXREG16 : DTB_WS_MAXREG) ws_kernel
     }
 }
 
-// =====================================================================================
-// Group-bound kernel (gb_kernel, Sauvola with 0 < k <= 1).  Warp-specialised like ws_kernel
-// (same ring, same READY/FREE hand-off), with a leaner column phase and a different output
-// phase:
-//
-// * Residue-decimated prefix layout.  Word k of a prefix array (k in [0, NC]; word k = sum of
-//   strip columns [0, k)) lives in plane rho = k & 3 at dec index m = k >> 2.  Dec index m
-//   belongs to column lane t = m >> 3, half hh = (m >> 2) & 1, element m & 3, stored at
-//   plane + 4*(hh*(T+1) + t) + (m & 3) (T column lanes).  A column lane writes its 32 words
-//   as 8 STS.128 (two per plane) and an output lane reads every 4th word of a run -- the only
-//   words the group bounds need -- as 2-3 LDS.128 per stream.  Both are bank-conflict free.
-//
-// * Group bounds.  For 4 adjacent outputs x0..x0+3 the window sums satisfy, because the
-//   column sums are >= 0 (prefix words are nondecreasing),
-//       S_I <= S(x) <= S_U,   Q(x) <= Q_U
-//   with I = [x0+3-r, x0+r] (intersection of the 4 windows) and U = [x0-r, x0+3+r] (union):
-//       S_U = P[b+3] - P[a],  S_I = P[b] - P[a+3],  Q_U = PQ[b+3] - PQ[a]   (a, b: run starts).
-//   Sauvola's t = m (1-k) + (k/R) m s is nondecreasing in s and, for 0 <= 1-k, in m, so
-//       t_lo = m_lo (1-k) <= t <= t_hi = m_hi ((1-k) + (k/R) sqrt(Q_U/n_lo - m_lo^2))
-//   (m_lo = S_I/n_hi, m_hi = S_U/n_lo; n_lo..n_hi the pixels' counts).  Evaluated in fp32
-//   with directed slack (relative 2^-17 on every factor, 1e-4 absolute) the bounds also
-//   enclose the reference's fp64 threshold.  A pixel with f < ceil(t_lo) is black, one with
-//   f >= ceil(t_hi) is white (f is an integer); the compare runs on 16-bit SWAR lanes, four
-//   pixels per handful of instructions.  Pixels in [ceil(t_lo), ceil(t_hi)) are uncertain:
-//   their group is re-decided per pixel (exact S, Q from the prefix -> certified fp32 ->
-//   fp64 replay), out of line.  On document pages this is ~1e-5 of the groups at W=127.
-// =====================================================================================
-#ifndef GB_STAGES
-#define GB_STAGES 3  // with 128 registers: 4 CTAs per SM (C4: 0.498 vs 0.584 ms at 5 stages, 168 regs, 3 CTAs)
-#endif
-#ifndef DTB_GB_MAXREG
-#define DTB_GB_MAXREG 128
-#endif
-
-
-#ifndef GB_NCW
-#define GB_NCW 2  // column warps (= output warps) per CTA; NC = 1024 * GB_NCW strip columns
-#endif
-#define GB_NC (1024 * GB_NCW)
-// words of one residue plane: 2 rows of (T+1) chunks
-__host__ __device__ constexpr int gb_plane_words(int NC) { return 8 * (NC / 32 + 1); }
-
-__host__ __device__ inline size_t gb_smem_bytes(int NC) {
-    // 2 buffers x (S, Q) x 4 planes, warp totals, 2*NS mbarriers, NS stages x 3 row segments
-    return sizeof(uint32_t) * (16 * (size_t)gb_plane_words(NC) + 32) + 2 * GB_STAGES * sizeof(uint64_t) +
-           (size_t)GB_STAGES * 3 * NC;
-}
-
-// word k of a residue-decimated prefix array (rare paths only)
-__device__ __forceinline__ uint32_t gb_word(const uint32_t* arr, int PW, int T1, int k) {
-    const int m = k >> 2;
-    return arr[(k & 3) * PW + 4 * (((m >> 2) & 1) * T1 + (m >> 3)) + (m & 3)];
-}
-
-// 8 consecutive dec words m0..m0+7 of one plane, m0 = 8*t0 + D (D compile-time, 0..7)
-template <int D>
-__device__ __forceinline__ void gb_stream(const uint32_t* plane, int t0, int T1, uint32_t (&w)[8]) {
-    constexpr int MU = D & 3;
-    const uint32_t* c0 = plane + 4 * ((D < 4 ? 0 : T1) + t0);
-    const uint32_t* c1 = plane + 4 * ((D < 4 ? T1 : 0) + t0 + (D < 4 ? 0 : 1));
-    const uint32_t* c2 = plane + 4 * ((D < 4 ? 0 : T1) + t0 + 1);
-    uint32_t v[12];
-    {
-        const uint4 x = *reinterpret_cast<const uint4*>(c0);
-        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-        const uint4 y = *reinterpret_cast<const uint4*>(c1);
-        v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
-        if (MU) {
-            const uint4 z = *reinterpret_cast<const uint4*>(c2);
-            v[8] = z.x; v[9] = z.y; v[10] = z.z; v[11] = z.w;
-        } else {
-            v[8] = v[9] = v[10] = v[11] = 0;
-        }
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g) w[g] = v[MU + g];
-}
-
-// ceil(x) for x in (-0.5, 2^22) as a pair of 16-bit lanes (x, x): FADD.RP onto 2^23 leaves
-// 2^23 + ceil(x), whose bit pattern minus 0x4B000000 is ceil(x); the IMAD replicates it.
-__device__ __forceinline__ uint32_t gb_ceil2(float x) {
-    const uint32_t bits = __float_as_uint(__fadd_ru(x, 8388608.0f));
-    return bits * 0x10001u - 0x4B000000u * 0x10001u;
-}
-
-// Uncertain group of 4 pixels x0..x0+3 (gb_kernel), out of line.  First a tighter lower
-// bound: the window contains the group's intersection window I, and a subset's squared
-// deviations about its own mean bound the window's from below, so var >= (n_I/n) var_I
-// (var_I = Q_I/n_I - m_I^2, evaluated lowered) and t >= m_lo ((1-k) + (k/R) s_lo).  Pixels the
-// refined bounds still leave open get exact S, Q from the residue-decimated prefix, the
-// certified fp32 decision and, within tol, the reference fp64 replay.  All four bytes are
-// rewritten after the caller's vector stores (program order).
-__device__ __noinline__ void gb_fix_group(const uint32_t* sPS, const uint32_t* sPQ, int PW, int T1,
-                                          int a_word, int b_word, const uint8_t* f4, uint8_t* orow,
-                                          int x0, int cols, int ny, int r, float cA, float cC,
-                                          float ca, float cc, float tol, double kk, double rr) {
-    const float kUp = 1.0f + 7.62939453125e-6f, kDn = 1.0f - 7.62939453125e-6f;  // 1 +- 2^-17
-    int nmin = 1 << 30, nmax = 0;
-    for (int i = 0; i < 4; ++i) {
-        const int x = x0 + i;
-        const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
-        nmin = min(nmin, nx); nmax = max(nmax, nx);
-    }
-    nmin = max(nmin, 1);
-    const float rlo = rcp_ftz((float)(ny * nmin)) * kUp, rhi = rcp_ftz((float)(ny * nmax)) * kDn;
-    const uint32_t pa0 = gb_word(sPS, PW, T1, a_word), pa3 = gb_word(sPS, PW, T1, a_word + 3);
-    const uint32_t pb0 = gb_word(sPS, PW, T1, b_word), pb3 = gb_word(sPS, PW, T1, b_word + 3);
-    const uint32_t qa0 = gb_word(sPQ, PW, T1, a_word), qa3 = gb_word(sPQ, PW, T1, a_word + 3);
-    const uint32_t qb0 = gb_word(sPQ, PW, T1, b_word), qb3 = gb_word(sPQ, PW, T1, b_word + 3);
-    const float fSI = (float)(pb0 - pa3);
-    const float mhi = (float)(pb3 - pa0) * rlo, mlo = fSI * rhi;
-    const float v = __fmaf_rn((float)(qb3 - qa0), rlo, -(mlo * mlo));
-    const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sqrt_ftz(fmaxf(v, 0.f)), cc, ca), tol), 4096.f);
-    const int nxI = min(x0 + r, cols - 1) - max(x0 + 3 - r, 0) + 1;
-    float sl = 0.f;
-    if (nxI >= 1) {
-        const float nI = (float)(ny * nxI), rnI = rcp_ftz(nI);
-        const float mI = fSI * (rnI * kUp);
-        const float vI = __fmaf_rn((float)(qb0 - qa3), rnI * kDn, -(mI * mI));
-        sl = sqrt_ftz(fmaxf(vI, 0.f) * (nI * rhi));
-    }
-    const float tlo = __fmaf_rn(mlo, __fmaf_rn(sl, cc * kDn, ca), -tol);
-    for (int i = 0; i < 4; ++i) {
-        const int x = x0 + i;
-        if (x >= cols) break;
-        const uint32_t f = f4[i];
-        uint32_t white;
-        if ((float)f < tlo) {
-            white = 0u;
-        } else if ((float)f >= thi) {
-            white = 0xFFu;
-        } else {
-            const uint32_t S = gb_word(sPS, PW, T1, b_word + i) - gb_word(sPS, PW, T1, a_word + i);
-            const uint32_t Q = gb_word(sPQ, PW, T1, b_word + i) - gb_word(sPQ, PW, T1, a_word + i);
-            const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
-            const uint32_t n = (uint32_t)(ny * nx);
-            const float d = fast_diff<DTB_METHOD_SAUVOLA, true>(S, Q, f, n, cA, cC, ca, cc);
-            if (fabsf(d) >= tol) {
-                white = d < 0.f ? 0u : 0xFFu;
-            } else {
-                white = exact_white(S, Q, (double)n, f, DTB_METHOD_SAUVOLA, kk, rr);
-                if (unsigned long long* audit = g_fp32_audit) {
-                    atomicAdd(&audit[0], 1ull);
-                    if (white != (d < 0.f ? 0u : 0xFFu)) atomicAdd(&audit[1], 1ull);
-                }
-            }
-        }
-        orow[x] = (uint8_t)white;
-    }
-}
-
-// DTB_GB_TIMES=1 (debug): per-CTA start/end %globaltimer, printed by the launcher.
-__device__ unsigned long long g_gb_times[2 * 8192];
-__device__ int g_gb_times_on = 0;
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-// R16 = r & 15 (fixes every stream's alignment); interior rows/lanes use n = (2r+1)^2.
-// SEG: segmented input (dtb_binarize_segments, e.g. halo rows read in place from a
-// neighbour GPU's band over NVLink); a compile-time variant like ws_kernel's.
-template <int R16, bool SEG>
-__global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
-    constexpr int NS = GB_STAGES;
-    constexpr int ALPHA = (16 - R16) & 15;
-    constexpr int EB = (ALPHA + 2 * R16 + 1) & 31;  // (alpha + 2r + 1) mod 32
-    // compile-time dec offsets (mod 8) of the six streams
-    constexpr int D_A0 = (ALPHA >> 2) & 7, D_A3 = ((ALPHA + 3) >> 2) & 7;
-    constexpr int D_B0 = (EB >> 2) & 7, D_B3 = ((EB + 3) >> 2) & 7;
-    constexpr int R_A0 = ALPHA & 3, R_A3 = (ALPHA + 3) & 3, R_B0 = EB & 3, R_B3 = (EB + 3) & 3;
-    extern __shared__ __align__(128) uint32_t sm[];
-    constexpr int NC = GB_NC;  // GB_NCW column warps (the host launches with ncw = now = GB_NCW)
-    constexpr int PW = gb_plane_words(NC);
-    constexpr int T = NC / 32, T1 = T + 1;
-    uint32_t* sWS = sm + 16 * PW;  // [2][8] per-column-warp totals, double buffered
-    uint32_t* sWQ = sWS + 16;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sWS + 32);
-    uint64_t* empty = full + NS;
-    uint8_t* ring = reinterpret_cast<uint8_t*>(empty + NS);
-    const int ncw = p.ncw, now = p.now, nthr = 32 * (ncw + now);
-    const int bid = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
-    // Warp w issues from SM sub-partition w % 4, so fixed role slots put each role on two
-    // sub-partitions only; with role_div > 0, alternate groups of role_div CTAs swap the slots
-    // (column warps on sub-partitions 2, 3) so co-resident CTAs spread both roles.
-    const bool swap = p.role_div > 0 && ((bid / p.role_div) & 1);
-    const int t = swap ? (int)(threadIdx.x ^ (32u * GB_NCW)) : (int)threadIdx.x;  // ncw = now
-    const int lane = t & 31, warp = t >> 5;
-    const bool is_col = warp < ncw;
-    if (g_gb_times_on && t == 0 && bid < 8192) g_gb_times[2 * bid] = gtimer();
-    const uint8_t* in = p.in + (int64_t)blockIdx.z * p.img_stride;
-    const int X0 = (int)blockIdx.x * p.TW;
-    const int xc0 = X0 - p.r - ALPHA;
-    const int ya = p.out_begin + (int)blockIdx.y * p.TH;
-    const int yb = min(ya + p.TH, p.out_end);
-    if (ya >= yb) return;
-    const uint8_t* in0 = in - (int64_t)p.row0 * p.pitch;
-    const int c_lo = max(xc0, 0);
-    const int c_hi = min(xc0 + NC, p.cols);
-    const int c_hi16 = c_lo + ((max(c_hi - c_lo, 0)) & ~15);
-    const int f_hi = min(X0 + p.TW, p.cols);
-    const int f_hi16 = X0 + ((max(f_hi - X0, 0)) & ~15);
-    // Items: warm-up items first, each carrying up to three warm-up rows (in the entering,
-    // leaving and centre slots -- a warm-up row needs only its bytes), then one item per output
-    // row.  Packing triples the warm-up rows in flight on the 3-stage ring.
-    Items it;
-    it.g0 = max(ya - p.r, 0);
-    const int nwr = min(ya + p.r, p.H - 1) - it.g0 + 1;  // warm-up rows
-    it.nwarm = (nwr + 2) / 3;                             // warm-up items
-    it.ya = ya;
-    it.n = it.nwarm + (yb - ya);
-
-    {
-        uint4* r4 = reinterpret_cast<uint4*>(ring);
-        const int n16 = NS * 3 * NC / 16;
-        for (int i = t; i < n16; i += blockDim.x) r4[i] = make_uint4(0, 0, 0, 0);
-    }
-    if (t == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], ncw + now);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    const uint64_t pol_keep = make_policy(p.l2hint ? 2 : 0), pol_drop = make_policy(p.l2hint ? 1 : 0);
-    auto issue = [&](int k) {
-        const int s = k % NS;
-        if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
-        uint8_t* E = ring + (size_t)s * 3 * NC;
-        uint8_t* O = E + NC;
-        uint8_t* F = O + NC;
-        int ge, go = -1, gf = -1;
-        if (k < it.nwarm) {
-            // warm-up rows g0+3k .. g0+3k+2 into the E, O, F slots (full strip width each)
-            const uint32_t rowb = (uint32_t)(c_hi16 - c_lo);
-            const int g = it.g0 + 3 * k, cnt = min(3, it.g0 + nwr - g);
-            mbar_expect_tx(&full[s], (uint32_t)cnt * rowb);
-            for (int i = 0; i < cnt; ++i) {
-                uint8_t* D = E + i * NC;
-                if (rowb) bulk_g2s(D + (c_lo - xc0), row_at<SEG>(p, in0, g + i) + c_lo, rowb, &full[s], pol_keep);
-                for (int c = c_hi16; c < c_hi; ++c) D[c - xc0] = row_at<SEG>(p, in0, g + i)[c];
-            }
-            return;
-        } else {
-            const int y = it.ya + (k - it.nwarm);
-            gf = y;
-            ge = (k == it.nwarm) ? -1 : y + p.r;
-            go = (k == it.nwarm) ? -1 : y - p.r - 1;
-            if (ge >= p.H) ge = -1;
-        }
-        const uint32_t rowb = (uint32_t)(c_hi16 - c_lo), fb = (uint32_t)(f_hi16 - X0);
-        uint32_t bytes = 0;
-        if (ge >= 0) bytes += rowb;
-        if (go >= 0) bytes += rowb;
-        if (gf >= 0) bytes += fb;
-        mbar_expect_tx(&full[s], bytes);
-        if (ge >= 0 && rowb) bulk_g2s(E + (c_lo - xc0), row_at<SEG>(p, in0, ge) + c_lo, rowb, &full[s], pol_keep);
-        if (go >= 0 && rowb) bulk_g2s(O + (c_lo - xc0), row_at<SEG>(p, in0, go) + c_lo, rowb, &full[s], pol_drop);
-        if (gf >= 0 && fb) bulk_g2s(F, row_at<SEG>(p, in0, gf) + X0, fb, &full[s], pol_keep);
-        for (int c = c_hi16; c < c_hi; ++c) {
-            if (ge >= 0) E[c - xc0] = row_at<SEG>(p, in0, ge)[c];
-            if (go >= 0) O[c - xc0] = row_at<SEG>(p, in0, go)[c];
-        }
-        for (int c = f_hi16; c < f_hi; ++c)
-            if (gf >= 0) F[c - X0] = row_at<SEG>(p, in0, gf)[c];
-    };
-
-    // The producer is lane 0 of the first OUTPUT warp: it refills a ring slot once all four
-    // warps released it, so a column warp never blocks on the output warps' progress (a
-    // column-warp producer stalled READY(k) behind output row k-1).
-    const bool producer = (t == 32 * ncw);
-    if (is_col) {
-        // ===================== column warps =====================
-        uint32_t cS[32], cQ[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) { cS[j] = 0; cQ[j] = 0; }
-        for (int k = 0; k < it.nwarm; ++k) {
-            const int s = k % NS;
-            mbar_wait(&full[s], (k / NS) & 1);
-            const int cnt = min(3, nwr - 3 * k);
-            for (int i = 0; i < cnt; ++i) {
-                const uint4* E = reinterpret_cast<const uint4*>(ring + (size_t)s * 3 * NC + i * NC + 32 * t);
-                uint32_t w[8];
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const uint4 a = E[q];
-                    w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
-                }
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t v = byte_at(w, j);
-                    cS[j] += v;
-                    cQ[j] += v * v;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cnt(&empty[s], warp == 0 ? 1 + now : 1);
-        }
-
-        // quarter sums of the column sums (columns 8h..8h+7), then kept incrementally with dp4a
-        uint32_t qS[4], qQ[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const int c = 8 * h;
-            qS[h] = ((cS[c] + cS[c + 1]) + (cS[c + 2] + cS[c + 3])) + ((cS[c + 4] + cS[c + 5]) + (cS[c + 6] + cS[c + 7]));
-            qQ[h] = ((cQ[c] + cQ[c + 1]) + (cQ[c + 2] + cQ[c + 3])) + ((cQ[c + 4] + cQ[c + 5]) + (cQ[c + 6] + cQ[c + 7]));
-        }
-        for (int k = it.nwarm; k < it.n; ++k) {
-            const int y = it.ya + (k - it.nwarm);
-            const int s = k % NS;
-            const int b = (k - it.nwarm) & 1;
-            mbar_wait(&full[s], (k / NS) & 1);
-            const uint8_t* stage = ring + (size_t)s * 3 * NC;
-            const bool first = (k == it.nwarm);
-            const bool ein = !first && y + p.r < p.H, oin = !first && y - p.r - 1 >= 0;
-            // entering / leaving row bytes of this lane's 32 columns (zero when outside the image)
-            uint32_t e[8], o[8];
-            {
-                const uint4* E = reinterpret_cast<const uint4*>(stage + 32 * t);
-                const uint4* O = reinterpret_cast<const uint4*>(stage + NC + 32 * t);
-                if (ein && oin) {
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const uint4 a = E[q], bb = O[q];
-                        e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
-                        o[4 * q] = bb.x; o[4 * q + 1] = bb.y; o[4 * q + 2] = bb.z; o[4 * q + 3] = bb.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const uint4 a = ein ? E[q] : make_uint4(0, 0, 0, 0);
-                        const uint4 bb = oin ? O[q] : make_uint4(0, 0, 0, 0);
-                        e[4 * q] = a.x; e[4 * q + 1] = a.y; e[4 * q + 2] = a.z; e[4 * q + 3] = a.w;
-                        o[4 * q] = bb.x; o[4 * q + 1] = bb.y; o[4 * q + 2] = bb.z; o[4 * q + 3] = bb.w;
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with item k's rows
-            // quarter totals (dp4a) -> lane total -> warp scan; the scan's shuffle latency and
-            // the column-warp hand-off overlap the vertical update below
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                qS[h] = dp4a_sub(o[2 * h + 1], dp4a_sub(o[2 * h], __dp4a(e[2 * h + 1], 0x01010101u,
-                                                      __dp4a(e[2 * h], 0x01010101u, qS[h]))));
-                qQ[h] += __dp4a(e[2 * h + 1], e[2 * h + 1], __dp4a(e[2 * h], e[2 * h], 0u)) -
-                         __dp4a(o[2 * h + 1], o[2 * h + 1], __dp4a(o[2 * h], o[2 * h], 0u));
-            }
-            const uint32_t TS = (qS[0] + qS[1]) + (qS[2] + qS[3]);
-            const uint32_t TQ = (qQ[0] + qQ[1]) + (qQ[2] + qQ[3]);
-            uint32_t iS = TS, iQ = TQ;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
-                const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
-                if (lane >= off) { iS += vs; iQ += vq; }
-            }
-            // column warp 0 hands its total to warp 1 (ncw = 2): arrive now, warp 1 syncs later;
-            // with more column warps every warp publishes and all sync after the update
-            if (GB_NCW == 2 && warp == 0) {
-                if (lane == 31) { sWS[8 * b] = iS; sWQ[8 * b] = iQ; }
-                nbar_arrive(BAR_COLS, 32 * ncw);
-            }
-            if (GB_NCW > 2 && lane == 31) { sWS[8 * b + warp] = iS; sWQ[8 * b + warp] = iQ; }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t ev = byte_at(e, j), ov = byte_at(o, j);
-                cS[j] = cS[j] + ev - ov;
-                cQ[j] = cQ[j] + ev * ev - ov * ov;
-            }
-            uint32_t bS = iS - TS, bQ = iQ - TQ;
-            if (GB_NCW > 2) {
-                nbar_sync(BAR_COLS, 32 * ncw);
-#pragma unroll
-                for (int w = 0; w < GB_NCW - 1; ++w)
-                    if (w < warp) { bS += sWS[8 * b + w]; bQ += sWQ[8 * b + w]; }
-            } else if (warp == 1) {
-                nbar_sync(BAR_COLS, 32 * ncw);
-                bS += sWS[8 * b]; bQ += sWQ[8 * b];
-            }
-            // wait until the output warps have consumed row k-2 from this prefix buffer
-            nbar_sync(BAR_FREE0 + b, nthr);
-            uint32_t* sPS = sm + (2 * b) * 4 * PW + 4 * t;
-            uint32_t* sPQ = sPS + 4 * PW;
-            // exclusive running prefix, stored residue-decimated: half hh of the lane's columns
-            // (two quarter chains) -> plane rho chunk (hh, t) = {pre[16hh+rho+4i], i = 0..3}
-            {
-                uint32_t cb0S = bS, cb0Q = bQ;
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    uint32_t c1S = cb0S + qS[2 * hh], c1Q = cb0Q + qQ[2 * hh];
-                    uint32_t vS[4][4], vQ[4][4];  // [rho][i]
-                    uint32_t r0S = cb0S, r0Q = cb0Q, r1S = c1S, r1Q = c1Q;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int j0 = 16 * hh + i, j1 = j0 + 8;
-                        vS[i & 3][i >> 2] = r0S; vQ[i & 3][i >> 2] = r0Q;
-                        vS[i & 3][2 + (i >> 2)] = r1S; vQ[i & 3][2 + (i >> 2)] = r1Q;
-                        r0S += cS[j0]; r0Q += cQ[j0];
-                        r1S += cS[j1]; r1Q += cQ[j1];
-                    }
-#pragma unroll
-                    for (int rho = 0; rho < 4; ++rho) {
-                        const int pos = rho * PW + 4 * hh * T1;
-                        *reinterpret_cast<uint4*>(&sPS[pos]) = make_uint4(vS[rho][0], vS[rho][1], vS[rho][2], vS[rho][3]);
-                        *reinterpret_cast<uint4*>(&sPQ[pos]) = make_uint4(vQ[rho][0], vQ[rho][1], vQ[rho][2], vQ[rho][3]);
-                    }
-                    cb0S = c1S + qS[2 * hh + 1]; cb0Q = c1Q + qQ[2 * hh + 1];
-                }
-                if (t == 32 * ncw - 1) {  // word NC: plane 0, dec index 8T -> chunk (0, T)
-                    sPS[4] = cb0S;
-                    sPQ[4] = cb0Q;
-                }
-            }
-            nbar_arrive(BAR_READY0 + b, nthr);
-        }
-        const int rows = it.n - it.nwarm;
-        if (rows >= 1) nbar_sync(BAR_FREE0 + (rows & 1), nthr);
-        if (rows >= 2) nbar_sync(BAR_FREE0 + ((rows + 1) & 1), nthr);
-    } else {
-        // ===================== output warps =====================
-        const int to = t - 32 * ncw;
-        const int xo = X0 + 32 * to;
-        const bool has_out = (32 * to + 32 + 2 * p.r + ALPHA <= NC) && (32 * to < p.TW) && (xo < p.cols);
-        const bool out_full = has_out && (xo + 32 <= p.cols) &&
-                              ((reinterpret_cast<uintptr_t>(p.bin) | (uintptr_t)p.bin_pitch |
-                                (uintptr_t)p.out_stride) & 15) == 0;
-        const bool x_interior = (xo - p.r >= 0) && (xo + 31 + p.r <= p.cols - 1);
-        const bool border_warp = __any_sync(0xffffffffu, has_out && !x_interior);
-        const int qB = (ALPHA + 2 * p.r + 1) >> 5;  // lane offset of the B streams
-        const int qB3 = (ALPHA + 2 * p.r + 4) >> 5;
-        const float W = (float)(2 * p.r + 1);
-        const float a1 = p.a, cK = p.c;  // 1-k, k/R
-        const float kUp = 1.0f + 7.62939453125e-6f, kDn = 1.0f - 7.62939453125e-6f;  // 1 +- 2^-17
-        const float dAbs = p.tol;  // >= the reference's own fp64 error on t (slide_constants)
-        uint8_t* obase = p.bin + (int64_t)blockIdx.z * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
-        nbar_arrive(BAR_FREE0, nthr);  // both prefix buffers start free
-        nbar_arrive(BAR_FREE0 + 1, nthr);
-        int issued = 0;
-        if (producer) {  // the ring's first NS items, then every warm-up slot as it frees up
-            while (issued < min(NS, it.n)) issue(issued++);
-            while (issued < min(it.nwarm + NS - 1, it.n)) issue(issued++);
-        }
-        for (int k = it.nwarm; k < it.n; ++k) {
-            const int y = it.ya + (k - it.nwarm);
-            const int s = k % NS;
-            const int b = (k - it.nwarm) & 1;
-            nbar_sync(BAR_READY0 + b, nthr);
-            // every warp released item k-1 by now (output warps: program order before READY(k);
-            // column warps: before READY(k-1)), so refilling its slot never blocks
-            if (producer)
-                while (issued < min(k + NS, it.n)) issue(issued++);
-            mbar_wait(&full[s], (k / NS) & 1);  // (complete; makes the staged rows visible)
-            const uint8_t* stage = ring + (size_t)s * 3 * NC;
-            const uint32_t* sPS = sm + (2 * b) * 4 * PW;
-            const uint32_t* sPQ = sPS + 4 * PW;
-            if (has_out) {
-                uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
-                const int ny = min(y + p.r, p.H - 1) - max(y - p.r, 0) + 1;
-                const uint8_t* fsm = stage + 2 * NC + 32 * to;
-                uint32_t fw[8];
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(fsm + 16 * q);
-                    fw[4 * q] = v.x; fw[4 * q + 1] = v.y; fw[4 * q + 2] = v.z; fw[4 * q + 3] = v.w;
-                }
-                uint32_t SA0[8], SA3[8], SB0[8], SB3[8], QA0[8], QB3[8];
-                gb_stream<D_A0>(sPS + R_A0 * PW, to, T1, SA0);
-                gb_stream<D_A3>(sPS + R_A3 * PW, to, T1, SA3);
-                gb_stream<D_B0>(sPS + R_B0 * PW, to + qB, T1, SB0);
-                gb_stream<D_B3>(sPS + R_B3 * PW, to + qB3, T1, SB3);
-                gb_stream<D_A0>(sPQ + R_A0 * PW, to, T1, QA0);
-                gb_stream<D_B3>(sPQ + R_B3 * PW, to + qB3, T1, QB3);
-                // 1/n for the row (interior lanes: n = ny * W for every pixel), with the slack;
-                // the intersection window I has n_I = ny (2r-2) pixels
-                const float rnr = rcp_ftz((float)ny * W);  // rel. error << the 2^-17 slack
-                const float rloR = rnr * kUp, rhiR = rnr * kDn;
-                uint32_t ow[8];
-                uint32_t um = 0;  // groups with an uncertain pixel
-                // rlo / rhi: 1/n_lo, 1/n_hi with the slack
-                auto group = [&](int g, float rlo, float rhi) {
-                    const uint32_t SU = SB3[g] - SA0[g];
-                    const uint32_t SI = SB0[g] - SA3[g];
-                    const uint32_t QU = QB3[g] - QA0[g];
-                    const float fSI = (float)SI;
-                    const float mhi = (float)SU * rlo;
-                    const float mlo = fSI * rhi;
-                    // upper: var <= Q_U/n_lo - m_lo^2 (raised)
-                    const float v = __fmaf_rn((float)QU, rlo, -(mlo * mlo));
-                    const float sd = sqrt_ftz(fmaxf(v, 0.f));
-                    const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sd, cK, a1), dAbs), 4096.f);
-                    const float tlo = __fmaf_rn(mlo, a1, -dAbs);
-                    const uint32_t H2 = gb_ceil2(thi), L2 = gb_ceil2(tlo);
-                    // SWAR: 16-bit lanes (f | 0x8000) - T: bit 15 set iff f >= T
-                    const uint32_t f4 = fw[g];
-                    const uint32_t fA = prmt(f4, 0x80808080u, 0x4240);  // pixels 0, 2
-                    const uint32_t fB = prmt(f4, 0x80808080u, 0x4341);  // pixels 1, 3
-                    const uint32_t wA = fA - H2, wB = fB - H2;
-                    ow[g] = prmt(wA, wB, 0xFBD9);  // bytes 0xFF where f >= ceil(t_hi)
-                    const uint32_t u = ((fA - L2) & ~wA) | ((fB - L2) & ~wB);
-                    if (u & 0x80008000u) um |= 1u << g;
-                };
-                if (!border_warp) {
-#pragma unroll
-                    for (int g = 0; g < 8; ++g) group(g, rloR, rhiR);
-                } else {
-                    // a warp with image-edge lanes: every lane takes per-group counts (warp-uniform)
-#pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        int nmin = 1 << 30, nmax = 0;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const int x = xo + 4 * g + i;
-                            const int nx = min(x + p.r, p.cols - 1) - max(x - p.r, 0) + 1;
-                            nmin = min(nmin, nx); nmax = max(nmax, nx);
-                        }
-                        nmin = max(nmin, 1);
-                        group(g, rcp_ftz((float)(ny * nmin)) * kUp, rcp_ftz((float)(ny * nmax)) * kDn);
-                    }
-                }
-                if (out_full) {
-#pragma unroll
-                    for (int q = 0; q < 2; ++q)
-                        __stcs(reinterpret_cast<uint4*>(orow + xo + 16 * q),
-                               make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]));
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int x = xo + j;
-                        if (x < p.cols) orow[x] = (uint8_t)(ow[j >> 2] >> (8 * (j & 3)));
-                    }
-                }
-                // Uncertain groups, out of line and after the vector stores (program order): each
-                // round, every lane with a flagged group re-decides one of them per pixel.
-                const unsigned am = __activemask();  // the lanes with outputs
-                while (__builtin_expect(__any_sync(am, um != 0u), 0)) {
-                    if (um) {
-                        const int g = __ffs(um) - 1;
-                        um &= um - 1;
-                        gb_fix_group(sPS, sPQ, PW, T1, ALPHA + 32 * to + 4 * g,
-                                     ALPHA + 2 * p.r + 1 + 32 * to + 4 * g, fsm + 4 * g, orow,
-                                     xo + 4 * g, p.cols, ny, p.r, p.cA, p.cC, p.a, p.c, p.tol, p.k, p.rr);
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            nbar_arrive(BAR_FREE0 + b, nthr);
-        }
-    }
-    if (g_gb_times_on && bid < 8192) {
-        __syncthreads();
-        if (t == 0) g_gb_times[2 * bid + 1] = gtimer();
-    }
-}
-
 // Certified tolerance (see header comment):  |t_fp32 - t_exact| <= E_fast and
 // |t_reference - t_exact| <= E_ref, so |f - t_fp32| >= tol = 2 (E_fast + E_ref) fixes the sign of
 // f - t_reference.  E_ref: the reference's var = Q/n - mean^2 carries <= 5u Q/n <= 3.6e-11
@@ -1664,8 +896,8 @@ __global__ void __maxnreg__(DTB_GB_MAXREG) gb_kernel(SlideParams p) {
 // rounding of D, sqrt.approx / rcp.approx (<= 2^-21 assumed each), the rounded constants and
 // the fmas give a relative error <= 1.1e-6 on the threshold; we use 1.5e-6 times a bound on |t|.
 void slide_constants(SlideParams& p) {
-    const char* env = getenv("DTB_L2HINT");
-    p.l2hint = env ? atoi(env) : 1;
+    static const int l2hint = [] { const char* e = getenv("DTB_L2HINT"); return e ? atoi(e) : 1; }();
+    p.l2hint = l2hint;
     const double W = 2.0 * p.r + 1.0;
     const FastConsts fc = fast_constants(p.method, p.k, p.rr, W * W);
     p.N = fc.N;
@@ -1679,20 +911,42 @@ void slide_constants(SlideParams& p) {
 // Host-side launch state is cached per instantiation: the dynamic-smem opt-in is raised once to
 // the largest size ever requested, and occupancy answers are memoised per (block, smem) -- the
 // runtime queries cost tens of microseconds, which would dominate small images.
-template <int V, int RXM4, int METHOD>
-static cudaError_t ensure_smem(size_t smem) {
-    static size_t granted = 48 * 1024;
-    if (smem <= granted) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(slide_kernel<V, RXM4, METHOD>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) granted = smem;
-    return e;
+// Per-device launch state of one kernel: the dynamic-smem opt-in (cudaFuncSetAttribute applies
+// to the current device only) and memoised occupancy answers (the runtime queries cost tens of
+// microseconds, which would dominate small images).  Keyed by (device, kernel[, block, smem]),
+// guarded by a mutex: the C ABI may be called from several host threads and devices.
+static std::mutex g_launch_mu;
+static std::map<std::pair<int, const void*>, size_t> g_granted;
+static std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
+
+static cudaError_t kernel_prepare(const void* fn, int nt, size_t smem, int* occ) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    size_t& g = g_granted[{dev, fn}];
+    if (smem > 48 * 1024 && smem > g) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        g = smem;
+    }
+    if (occ) {
+        auto it = g_occ.find({dev, fn, nt, smem});
+        if (it == g_occ.end()) {
+            int blocks = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, nt, smem) != cudaSuccess)
+                blocks = 1;
+            it = g_occ.emplace(std::make_tuple(dev, fn, nt, smem), std::max(blocks, 1)).first;
+        }
+        *occ = it->second;
+    }
+    return cudaSuccess;
 }
 
 template <int V, int RXM4, int METHOD>
 static cudaError_t run_slide(dim3 grid, int nt, size_t smem, const SlideParams& p,
                              cudaStream_t st) {
-    cudaError_t e = ensure_smem<V, RXM4, METHOD>(smem);
+    cudaError_t e = kernel_prepare((const void*)slide_kernel<V, RXM4, METHOD>, nt, smem, nullptr);
     if (e != cudaSuccess) return e;
     slide_kernel<V, RXM4, METHOD><<<grid, nt, smem, st>>>(p);
     return cudaGetLastError();
@@ -1700,21 +954,8 @@ static cudaError_t run_slide(dim3 grid, int nt, size_t smem, const SlideParams& 
 
 template <int V, int RXM4, int METHOD>
 static int occupancy(int nt, size_t smem) {
-    static int cache_nt[16], cache_occ[16];
-    static size_t cache_smem[16];
-    static int n_cached = 0;
-    for (int i = 0; i < n_cached; ++i)
-        if (cache_nt[i] == nt && cache_smem[i] == smem) return cache_occ[i];
-    int blocks = 0;
-    ensure_smem<V, RXM4, METHOD>(smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, slide_kernel<V, RXM4, METHOD>, nt,
-                                                      smem) != cudaSuccess)
-        blocks = 1;
-    blocks = std::max(blocks, 1);
-    if (n_cached < 16) {
-        cache_nt[n_cached] = nt; cache_smem[n_cached] = smem; cache_occ[n_cached] = blocks;
-        ++n_cached;
-    }
+    int blocks = 1;
+    kernel_prepare((const void*)slide_kernel<V, RXM4, METHOD>, nt, smem, &blocks);
     return blocks;
 }
 
@@ -1752,50 +993,13 @@ static cudaError_t dispatch_rx(int m, bool sv, dim3 grid, int nt, size_t smem,
     return cudaErrorInvalidValue;
 }
 
-// DTB_PLAN_TIE=1: on equal staged work prefer more column warps per strip (fewer strips);
-// measured neutral (C3 -1%, C5 W163/W179 +4%), so the default keeps the narrowest plan
-static bool plan_tie_wide() {
-    static int v = -1;
-    if (v < 0) { const char* e = getenv("DTB_PLAN_TIE"); v = e ? atoi(e) : 0; }
-    return v == 1;
-}
-
-// DTB_SLIDE_V=16 / 32 forces the columns per thread of the sliding kernels; unset = auto
-static int slide_v() {
-    static int v = -1;
-    if (v < 0) {
-        const char* env = getenv("DTB_SLIDE_V");
-        v = env ? (atoi(env) == 16 ? 16 : 32) : 0;
-    }
-    return v;
-}
-
-
 // ---- warp-specialized launcher
 template <int V, int VO, int RXM4, int MX>
 static cudaError_t ws_run(dim3 grid, int nt, size_t smem, const SlideParams& p, cudaStream_t st,
                           int* occ) {
-    static size_t granted = 48 * 1024;
     auto kern = ws_kernel<V, VO, RXM4, MX>;
-    if (smem > granted) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        granted = smem;
-    }
-    if (occ) {
-        static int c_nt[16], c_occ[16];
-        static size_t c_smem[16];
-        static int nc = 0;
-        for (int i = 0; i < nc; ++i)
-            if (c_nt[i] == nt && c_smem[i] == smem) { *occ = c_occ[i]; return cudaSuccess; }
-        int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nt, smem) != cudaSuccess)
-            blocks = 1;
-        *occ = std::max(blocks, 1);
-        if (nc < 16) { c_nt[nc] = nt; c_smem[nc] = smem; c_occ[nc] = *occ; ++nc; }
-        return cudaSuccess;
-    }
+    cudaError_t e = kernel_prepare((const void*)kern, nt, smem, occ);
+    if (e != cudaSuccess || occ) return e;
     kern<<<grid, nt, smem, st>>>(p);
     return cudaGetLastError();
 }
@@ -1818,100 +1022,20 @@ static cudaError_t ws_dispatch_vo(int m, bool sv, dim3 grid, int nt, size_t smem
 #undef DTB_WS_M
 }
 
-// V = VO = 16 variant (DTB_WS_V16=1): half the per-thread state, twice the warps
-static int ws_v16() {
-    static int v = -1;
-    if (v < 0) { const char* e = getenv("DTB_WS_V16"); v = e ? atoi(e) : DTB_WS_V16_DEFAULT; }
-    return v;
-}
-
 static cudaError_t ws_dispatch(int m, bool sv, dim3 grid, int nt, size_t smem, const SlideParams& p,
-                               cudaStream_t st, int* occ, bool v16) {
-    if (v16) return ws_dispatch_vo<16, 16>(m, sv, grid, nt, smem, p, st, occ);
+                               cudaStream_t st, int* occ) {
     return ws_dispatch_vo<32, 32>(m, sv, grid, nt, smem, p, st, occ);
 }
 
-static int use_ws() {
-    static int v = -1;
-    if (v < 0) {
-        const char* env = getenv("DTB_WS");
-        v = env ? atoi(env) : DTB_WS_DEFAULT;
-    }
+static int use_ws() {  // DTB_WS=0/1 forces the classic / warp-specialised kernel (read once)
+    static const int v = [] { const char* e = getenv("DTB_WS"); return e ? atoi(e) : DTB_WS_DEFAULT; }();
     return v;
 }
 
-// Debug / tuning knobs read once: DTB_PRINT_PLAN=1 prints each launch's strip/band plan;
-// DTB_BAND_SCALE scales the band count (1 = one full wave of resident CTAs).
+// Debug: DTB_PRINT_PLAN=1 prints each launch's strip/band plan (read once)
 static bool print_plan() {
-    static int v = -1;
-    if (v < 0) { const char* e = getenv("DTB_PRINT_PLAN"); v = (e && e[0] == '1') ? 1 : 0; }
-    return v == 1;
-}
-static double band_scale() {
-    static double v = -1.0;
-    if (v < 0) { const char* e = getenv("DTB_BAND_SCALE"); v = e ? atof(e) : 1.0; if (!(v > 0)) v = 1.0; }
+    static const bool v = [] { const char* e = getenv("DTB_PRINT_PLAN"); return e && e[0] == '1'; }();
     return v;
-}
-
-// ---- group-bound launcher (gb_kernel)
-template <int R16, bool SEG>
-static cudaError_t gb_run(dim3 grid, int nt, size_t smem, const SlideParams& p, cudaStream_t st,
-                          int* occ) {
-    static size_t granted = 48 * 1024;
-    auto kern = gb_kernel<R16, SEG>;
-    if (smem > granted) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        granted = smem;
-    }
-    if (occ) {
-        static int c_nt[16], c_occ[16];
-        static size_t c_smem[16];
-        static int nc = 0;
-        for (int i = 0; i < nc; ++i)
-            if (c_nt[i] == nt && c_smem[i] == smem) { *occ = c_occ[i]; return cudaSuccess; }
-        int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nt, smem) != cudaSuccess)
-            blocks = 1;
-        *occ = std::max(blocks, 1);
-        if (nc < 16) { c_nt[nc] = nt; c_smem[nc] = smem; c_occ[nc] = *occ; ++nc; }
-        return cudaSuccess;
-    }
-    kern<<<grid, nt, smem, st>>>(p);
-    return cudaGetLastError();
-}
-
-static cudaError_t gb_dispatch(int r16, dim3 grid, int nt, size_t smem, const SlideParams& p,
-                               cudaStream_t st, int* occ) {
-    switch (r16) {
-#define DTB_GB_CASE(R) case R: return p.nseg ? gb_run<R, true>(grid, nt, smem, p, st, occ) \
-                                              : gb_run<R, false>(grid, nt, smem, p, st, occ);
-        DTB_GB_CASE(0) DTB_GB_CASE(1) DTB_GB_CASE(2) DTB_GB_CASE(3)
-        DTB_GB_CASE(4) DTB_GB_CASE(5) DTB_GB_CASE(6) DTB_GB_CASE(7)
-        DTB_GB_CASE(8) DTB_GB_CASE(9) DTB_GB_CASE(10) DTB_GB_CASE(11)
-        DTB_GB_CASE(12) DTB_GB_CASE(13) DTB_GB_CASE(14) DTB_GB_CASE(15)
-#undef DTB_GB_CASE
-    }
-    return cudaErrorInvalidValue;
-}
-
-// DTB_GB: 0 never, 1 whenever eligible, 2 (default) eligible and r >= DTB_GB_MIN_R.
-#ifndef DTB_GB_MIN_R
-#define DTB_GB_MIN_R 31
-#endif
-#ifndef DTB_GB_MIN_COLS
-#define DTB_GB_MIN_COLS 1536
-#endif
-// Auto mode also wants a large page: on 4096^2 pages with sigma-12 noise (C5) many groups need
-// the out-of-line re-decision and the one-wave plan has ~20-row bands under 2r+1 warm-up rows,
-// which measured 1.1-1.3x slower than ws_kernel at W 67..179 (profiles/r01d_config_table.json).
-#ifndef DTB_GB_MIN_PIXELS
-#define DTB_GB_MIN_PIXELS (1ll << 26)
-#endif
-static int gb_mode() {  // read per launch (tests switch it)
-    const char* e = getenv("DTB_GB");
-    return e ? atoi(e) : 2;
 }
 
 static thread_local const char* g_last_kernel = "";
@@ -1940,36 +1064,25 @@ static int bb_mode() {  // read per launch (tests switch it)
 }
 
 // Band count minimising waves * (TH + wf (2r+1)) + tf * TH in main-row units per CTA slot
-// (see the gb_kernel launcher); DTB_BAND_SCALE overrides with scale x one wave.
+// (bb_kernel's planner uses the same model).
 static int plan_bands(int rows_out, int units, int slots, int r, double wf, double tf) {
     int nbands = 1;
-    if (getenv("DTB_BAND_SCALE")) {
-        nbands = std::max(1, (int)(band_scale() * slots / std::max(1, units)));
-    } else {
-        double best_cost = 1e300;
-        const int nb_max = std::max(1, std::min((rows_out + 7) / 8, 4 * slots / std::max(1, units) + 1));
-        for (int nb = 1; nb <= nb_max; ++nb) {
-            const int th = (rows_out + nb - 1) / nb;
-            const int waves = (units * nb + slots - 1) / slots;
-            const double cost = waves * (th + wf * (2 * r + 1)) + tf * th;
-            if (cost < best_cost) { best_cost = cost; nbands = nb; }
-        }
+    double best_cost = 1e300;
+    const int nb_max = std::max(1, std::min((rows_out + 7) / 8, 4 * slots / std::max(1, units) + 1));
+    for (int nb = 1; nb <= nb_max; ++nb) {
+        const int th = (rows_out + nb - 1) / nb;
+        const int waves = (units * nb + slots - 1) / slots;
+        const double cost = waves * (th + wf * (2 * r + 1)) + tf * th;
+        if (cost < best_cost) { best_cost = cost; nbands = nb; }
     }
     return std::max(1, std::min(nbands, (rows_out + 7) / 8));
 }
 
-static int slide_band_model() {  // DTB_BAND_MODEL=0: one full wave (the previous rule)
-    static int v = -1;
-    if (v < 0) { const char* e = getenv("DTB_BAND_MODEL"); v = e ? atoi(e) : 1; }
-    return v;
-}
-
 cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t st) {
     slide_constants(p);
-    const int vset = slide_v();
     // segmented variants: V = 32 only; the tmap variant runs V = 16 (half the registers per
     // thread: twice the resident warps for its fp64 epilogue)
-    int V = p.tmap ? 16 : (p.nseg ? 32 : (vset ? vset : 32));
+    int V = p.tmap ? 16 : 32;
     const int rows_out = p.out_end - p.out_begin;
     const int alpha = (16 - (p.rx & 15)) & 15;
     // strip plan: w warps -> NC = 32 V w columns; pick the w (1..8) with the least total column
@@ -1984,7 +1097,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
             const int ns = (p.cols + twmax - 1) / twmax;
             const int tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
             const long work = (long)ns * nc;
-            if (b.w == 0 || work < b.work || (plan_tie_wide() && work == b.work)) b = Plan{w, ns, tw, work};
+            if (b.w == 0 || work < b.work) b = Plan{w, ns, tw, work};
         }
         return b;
     };
@@ -1998,88 +1111,11 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     Plan pl = plan_for(V);
     int best_w = pl.w, best_strips = pl.strips, best_tw = pl.tw;
     if (best_w == 0) return cudaErrorInvalidValue;  // window too wide for 8 warps (caller checks)
-    // group-bound kernel: Sauvola with 0 < k <= 1, strips of 2 column warps (see gb_kernel)
-    const int gbm = gb_mode();
-    const int gb_tw = 32 * ((GB_NC - 2 * p.rx - alpha) / 32);
-    // r <= 127: the union window's Q_U (2r+4 columns) stays below 2^32 (65025 * 258 * 255);
-    // slide_ok alone admits W = 257, whose union sums could wrap
-    if (V == 32 && p.method == DTB_METHOD_SAUVOLA && p.k > 0.0 && p.k <= 1.0 &&
-        p.rx == p.r && p.r <= 127 && gb_tw >= 32 &&
-        (gbm == 1 || (gbm == 2 && p.r >= DTB_GB_MIN_R && p.cols >= DTB_GB_MIN_COLS &&
-                      (long long)p.cols * (p.out_end - p.out_begin) * n_images >= DTB_GB_MIN_PIXELS))) {
-        const int ns = (p.cols + gb_tw - 1) / gb_tw;
-        best_strips = ns;
-        best_tw = 32 * ((p.cols + 32 * ns - 1) / (32 * ns));
-        best_w = GB_NCW;
-        p.ncw = best_w;
-        p.now = GB_NCW;  // (the role swap below pairs the two equal halves of the CTA)
-        {
-            const char* se = getenv("DTB_GB_SWAP");
-            p.role_div = (se && atoi(se) > 0) ? atoi(se) : 0;
-        }
-        p.NC = GB_NC;
-        p.TW = best_tw;
-        const int nt = 32 * (p.ncw + p.now);
-        const size_t smem = gb_smem_bytes(p.NC);
-        int occ = 1;
-        const cudaError_t qe = gb_dispatch(p.r & 15, dim3(), nt, smem, p, st, &occ);
-        if (qe != cudaSuccess) return qe;
-        const int slots = num_sms * occ;
-        // Band count from a cost model, in main-row units per CTA slot:
-        //   waves * (TH + 0.25 (2r+1))  +  0.3 TH
-        // (a warm-up row -- column sums only -- costs ~1/4 of a main row; the last term stands
-        // for the content-dependent spread of band cost: uncertain groups cluster in dark page
-        // regions, and a one-wave launch waits on its slowest bands).  C4: 2 waves of 125-row
-        // bands (0.498 ms vs 0.518 at one wave); 4096^2 pages: one wave (bands of 2r+1 rows of
-        // warm-up over ~20 output rows otherwise dominate).
-        int nbands = 1;
-        {
-            const char* bse = getenv("DTB_BAND_SCALE");
-            const int units = std::max(1, best_strips * n_images);
-            if (bse) {
-                nbands = std::max(1, (int)(band_scale() * slots / units));
-            } else {
-                double best_cost = 1e300;
-                const int nb_max = std::max(1, std::min((rows_out + 7) / 8, 4 * slots / units + 1));
-                for (int nb = 1; nb <= nb_max; ++nb) {
-                    const int th = (rows_out + nb - 1) / nb;
-                    const int waves = (units * nb + slots - 1) / slots;
-                    const double cost = waves * (th + 0.25 * (2 * p.r + 1)) + 0.3 * th;
-                    if (cost < best_cost) { best_cost = cost; nbands = nb; }
-                }
-            }
-            nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
-        }
-        p.TH = (rows_out + nbands - 1) / nbands;
-        dim3 grid(best_strips, (rows_out + p.TH - 1) / p.TH, n_images);
-        if (print_plan())
-            fprintf(stderr, "[dtb plan] gb_kernel cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d smem=%zu\n",
-                    p.cols, rows_out, p.r, best_w, best_strips, best_tw, occ, (int)grid.y, p.TH, smem);
-        g_last_kernel = "gb_kernel";
-        const char* tenv = getenv("DTB_GB_TIMES");
-        if (tenv && tenv[0] == '1') {
-            const int on = 1;
-            cudaMemcpyToSymbol(g_gb_times_on, &on, sizeof(on));
-            const cudaError_t e = gb_dispatch(p.r & 15, grid, nt, smem, p, st, nullptr);
-            cudaDeviceSynchronize();
-            static unsigned long long h[2 * 8192];
-            cudaMemcpyFromSymbol(h, g_gb_times, sizeof(h));
-            const int nb = std::min(8192, (int)(grid.x * grid.y * grid.z));
-            unsigned long long t0 = ~0ull, t1 = 0;
-            for (int i = 0; i < nb; ++i) { t0 = std::min(t0, h[2 * i]); t1 = std::max(t1, h[2 * i + 1]); }
-            fprintf(stderr, "[gb times] ctas=%d span=%.1f us\n", nb, (t1 - t0) * 1e-3);
-            for (int i = 0; i < nb; ++i)
-                fprintf(stderr, "[gb cta] %d strip=%d band=%d start=%.1f end=%.1f\n", i, i % (int)grid.x,
-                        (i / (int)grid.x) % (int)grid.y, (h[2 * i] - t0) * 1e-3, (h[2 * i + 1] - t0) * 1e-3);
-            return e;
-        }
-        return gb_dispatch(p.r & 15, grid, nt, smem, p, st, nullptr);
-    }
     // Auto V: 16 columns per thread give strips in 512-column steps (and 128-register warps);
     // take them when that cuts the staged column work by >= 10% (C2 pages 2480 wide: one strip
     // of 2560 instead of three of 1024 -- W15 0.119 -> 0.058 ms; C5 W3: 0.093 -> 0.078 ms;
     // C5 W67 / W131 within 2%).
-    if (!vset && !p.nseg && !p.tmap && V == 32) {
+    if (!p.nseg && !p.tmap && V == 32) {
         const Plan p16 = plan_for(16);
         if (p16.w > 0 && p16.work * 10 <= pl.work * 9) {
             V = 16;
@@ -2090,18 +1126,8 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // ms; single-column-warp strips such as C3's are faster on the classic kernel)
     const int ws_mode = use_ws();
     if (V == 32 && (ws_mode == 1 || (ws_mode == 2 && best_w >= 2))) {
-        const bool v16 = ws_v16() && best_w <= 4;  // column-warp totals table holds 8 warps
-        const int vo = v16 ? 16 : 32;
-        p.ncw = v16 ? 2 * best_w : best_w;
-        p.now = (best_tw + 32 * vo - 1) / (32 * vo);
-        {
-            static int swap_mode = -1;
-            if (swap_mode < 0) {
-                const char* env = getenv("DTB_WS_SWAP");
-                swap_mode = env ? atoi(env) : 0;  // measured: 0.656 vs 0.621 ms (C4) with it on
-            }
-            p.role_div = swap_mode ? num_sms : 0;
-        }
+        p.ncw = best_w;
+        p.now = (best_tw + 32 * 32 - 1) / (32 * 32);
         p.NC = 1024 * best_w;
         p.TW = best_tw;
         const int nt = 32 * (p.ncw + p.now);
@@ -2109,9 +1135,9 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         const int m = p.rx & 3;
         const bool sv = p.method == DTB_METHOD_SAUVOLA;
         int occ = 1;
-        ws_dispatch(m, sv, dim3(), nt, smem, p, st, &occ, v16);
+        ws_dispatch(m, sv, dim3(), nt, smem, p, st, &occ);
         const int slots = num_sms * occ;
-        int nbands = std::max(1, (int)(band_scale() * slots / std::max(1, best_strips * n_images)));
+        int nbands = std::max(1, slots / std::max(1, best_strips * n_images));
         nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));  // one wave (the model measured
                                                                      // 1-4% slower here, C5 W195+)
         p.TH = (rows_out + nbands - 1) / nbands;
@@ -2120,7 +1146,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
             fprintf(stderr, "[dtb plan] ws_kernel cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d\n",
                     p.cols, rows_out, p.r, best_w, best_strips, best_tw, occ, (int)grid.y, p.TH);
         g_last_kernel = "ws_kernel";
-        return ws_dispatch(m, sv, grid, nt, smem, p, st, nullptr, v16);
+        return ws_dispatch(m, sv, grid, nt, smem, p, st, nullptr);
     }
     const int nt = 32 * best_w;
     p.NC = V * nt;
@@ -2132,13 +1158,10 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     int occ = 1;
     if (V == 16) dispatch_rx<16>(m, sv, dim3(), nt, smem, p, st, &occ);
     else dispatch_rx<32>(m, sv, dim3(), nt, smem, p, st, &occ);
-    // bands: one full wave of resident CTAs (bands as tall as possible: the warm-up of each
-    // band costs 2r+1 rows of vertical work)
+    // cost-model band count (C3 0.949 -> 0.885 ms, C5 W19..W179 2-4% faster than one wave; a
+    // band's warm-up costs 2r+1 rows of vertical work)
     const int slots = num_sms * occ;
-    int nbands = std::max(1, (int)(band_scale() * slots / std::max(1, nstrips * n_images)));
-    nbands = std::max(1, std::min(nbands, (rows_out + 7) / 8));
-    // cost-model band count (C3 0.949 -> 0.885 ms, C5 W19..W179 2-4% faster than one wave)
-    if (slide_band_model()) nbands = plan_bands(rows_out, nstrips * n_images, slots, p.r, 0.25, 0.1);
+    const int nbands = plan_bands(rows_out, nstrips * n_images, slots, p.r, 0.25, 0.1);
     p.TH = (rows_out + nbands - 1) / nbands;
     dim3 grid(nstrips, (rows_out + p.TH - 1) / p.TH, n_images);
     if (print_plan())

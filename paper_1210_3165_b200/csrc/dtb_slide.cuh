@@ -31,7 +31,7 @@ struct SlideParams {
     const uint8_t* seg_ptr[3];
     int64_t seg_pitch[3];
     int seg_lo[3];
-    int role_div;      // ws: swap the two roles' warp slots in every other group of role_div CTAs (0 = never)
+
     // optional fp64 threshold map (slide_kernel TMAP variant): tmap + y * tmap_pitch (bytes)
     double* tmap;
     int64_t tmap_pitch;

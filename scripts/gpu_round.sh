@@ -1,0 +1,17 @@
+# Measurement bundle for one GPU call (writes gpurun_out/):
+#   bash scripts/gpu_round.sh TAG         smoke, GPU tests, bench (+ reference arm), config
+#                                          table, ncu launch list and one full capture of the
+#                                          C4 hot kernel
+set -u
+TAG=${1:-run}
+O=gpurun_out
+python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo smoke=$?
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/${TAG}_pytest_gpu.log 2>&1; echo pytest=$?
+timeout 600 python bench.py > $O/${TAG}_bench.log 2>&1; echo bench=$?
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/${TAG}_bench_ref.log 2>&1; echo ref=$?
+timeout 600 python bench.py --emulate-bands 8 --steps 10 --warmup 3 > $O/${TAG}_emul8.log 2>&1; echo emul=$?
+timeout 900 python scripts/config_table.py --reps 10 > $O/${TAG}_config_table.json 2> $O/${TAG}_config_table.err; echo table=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/${TAG}_launches.csv \
+  python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_ncu_launch.log 2>&1; echo launches=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"bb_kernel" -s 2 -c 1 -o $O/${TAG}_prof_bb \
+  python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_ncu.log 2>&1; echo ncu=$?
