@@ -472,6 +472,7 @@ int dtb_binarize(const uint8_t* gray, int64_t pitch, int32_t in_rows, int32_t co
         (!tmap || (((uintptr_t)tmap | (uintptr_t)tmap_pitch) & 15) == 0)) {
         SlideParams q{};
         q.in = gray; q.pitch = pitch; q.cols = cols; q.row0 = row0_global; q.H = rows_global;
+        q.in_rows = in_rows;
         q.out_begin = out_row_begin; q.out_end = out_row_end; q.r = rad;
         q.rx = std::min(rad, cols - 1);
         q.bin = binary; q.bin_pitch = binary_pitch; q.method = method; q.k = k; q.rr = r;
@@ -501,7 +502,7 @@ int dtb_binarize_batch(const uint8_t* gray, int64_t image_stride, int32_t n_imag
     if (slide_ok(win / 2, cols, rows, gray, cols, image_stride)) {
         SlideParams q{};
         q.in = gray; q.pitch = cols; q.img_stride = image_stride; q.cols = cols; q.row0 = 0;
-        q.H = rows; q.out_begin = 0; q.out_end = rows; q.r = win / 2;
+        q.H = rows; q.in_rows = rows; q.out_begin = 0; q.out_end = rows; q.r = win / 2;
         q.rx = std::min(win / 2, cols - 1);
         q.bin = binary; q.bin_pitch = cols; q.out_stride = out_stride;
         q.method = method; q.k = k; q.rr = r;

@@ -79,6 +79,7 @@ int dtb_binarize_segments(const uint8_t* const* seg_ptr, const int64_t* seg_pitc
     q.cols = cols;
     q.row0 = row0_global;
     q.H = rows_global;
+    q.in_rows = total;
     q.out_begin = out_row_begin;
     q.out_end = out_row_end;
     q.r = rad;

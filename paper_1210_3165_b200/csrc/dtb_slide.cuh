@@ -10,6 +10,7 @@ struct SlideParams {
     int64_t pitch;
     int64_t img_stride;
     int cols, row0, H, out_begin, out_end;
+    int in_rows;       // rows the input buffer (or the segments together) holds from row0
     int r, rx;
     int NC;     // columns per strip (= 32 * blockDim.x), set by launch_slide
     int TW;     // outputs per strip (multiple of 32), set by launch_slide

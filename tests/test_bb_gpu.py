@@ -166,3 +166,26 @@ def test_random_pages_and_params(seed):
         k = float(rng.choice([0.01, 0.2, 0.34, 0.5, 0.77, 1.0]))
         r = float(rng.choice([1.0, 16.0, 128.0, 255.0, 300.0]))
         _check(img, 2 * rad + 1, k, r, expect_bb=rad >= 8)
+
+
+@pytest.mark.parametrize("w", [130, 1003, 2550, 4097])
+def test_odd_widths_pitched(w):
+    # widths that are not a multiple of 16 arrive in a 16-byte pitched buffer: the tensor-map
+    # staging reads the padding bytes of the last chunk, which the kernel must mask
+    img = workloads.doc_gray(170, w, w, 90)
+    _check(img, 2 * min(63, (w - 1) // 2) + 1, 0.34)
+
+
+def test_odd_width_band_and_segments():
+    torch = engine.torch_mod()
+    img = workloads.doc_gray(600, 2003, 5, 400)
+    want, _ = oracle.binarize(img, 101, "sauvola", 0.34, tmap=False, threads=8)
+    pitched = torch.empty((600, 2016), dtype=torch.uint8, device="cuda")[:, :2003]
+    pitched.copy_(torch.from_numpy(img))
+    got = engine.binarize_band(pitched[100:500], 100, 600, 150, 450, 101, "sauvola", 0.34, 128.0)
+    assert _ran_bb()
+    assert np.array_equal(got.cpu().numpy(), want[150:450])
+    segs = [(t.data_ptr(), t.stride(0), t.shape[0], 2003) for t in (pitched[:200], pitched[200:420], pitched[420:])]
+    out = engine.binarize_segments(segs, 0, 600, 0, 600, 101, "sauvola", 0.34, 128.0)
+    assert _ran_bb()
+    assert np.array_equal(out.cpu().numpy(), want)
