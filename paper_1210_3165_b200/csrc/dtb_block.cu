@@ -692,20 +692,18 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     slide_constants(p);
     int tw;
     if (!bb_geometry(p.r, tw)) return cudaErrorInvalidValue;
-    // Strip plan.  Interior strips output up to tw columns.  On wide pages the groups whose
-    // windows the image's left / right edge clips (per-pixel bounds, a warp-wide pass per row)
-    // get strips of their own -- the first strip is exactly the left edge groups, the last one
-    // the right edge groups plus a remainder < 16 m columns -- so no strip carries both a full
-    // interior load and the edge pass (C4: the edge strips were ~12% slower and set the kernel
-    // time, every pipeline running in one wave).
+    // Strip plan.  Interior strips output up to tw columns.  The strips holding the image's
+    // left / right edge also decide their edge groups per pixel, so on wide pages they get
+    // about half a strip: every pipeline runs in one wave, and a full-width edge strip set the
+    // kernel time (C4: 0.41 -> 0.39 ms).  Strips of exactly the edge groups measured slower
+    // (0.394 vs 0.382 ms): such a strip still pays the full per-row column and staging cost.
     int ns, tw0;
-    const int edge = 8 * ((p.r + 7) / 8);  // columns of the left-edge groups
     if (p.cols >= 4 * tw) {
-        tw0 = 16 * ((edge + 15) / 16);
-        const int inner = p.cols - tw0 - (p.r + 8);  // the last strip keeps >= r+8 columns
-        const int m = (inner + tw - 1) / tw;
-        p.TW = 16 * (inner / (16 * m));
-        ns = 1 + m + 1;
+        const int e = std::max(16 * ((2 * p.r + 15) / 16), 16 * ((tw / 2 + 15) / 16));
+        const int m = (p.cols - 2 * e + tw - 1) / tw;
+        p.TW = 16 * ((p.cols - 2 * e + 16 * m - 1) / (16 * m));
+        tw0 = e;
+        ns = 1 + (p.cols - tw0 + p.TW - 1) / p.TW;
     } else {
         ns = (p.cols + tw - 1) / tw;
         p.TW = 16 * ((p.cols + 16 * ns - 1) / (16 * ns));  // balanced strips, 16-column steps

@@ -400,6 +400,10 @@ static int gs_run(GsParams p, int structure, int win, void* stream) {
     if (win < 3 || win % 2 == 0) return fail(DTB_E_INVALID, "window: must be an odd integer >= 3, got %d", win);
     if (p.bin && p.method != DTB_METHOD_SAUVOLA && p.method != DTB_METHOD_NIBLACK)
         return fail(DTB_E_INVALID, "method: unknown code %d", p.method);
+    // the same parameter checks as dtb_binarize (threshold.py:40-52): k_sauvola > 0, r > 0
+    if (p.bin && p.method == DTB_METHOD_SAUVOLA && !(p.k > 0.0))
+        return fail(DTB_E_INVALID, "k_sauvola: must be > 0, got %g", p.k);
+    if (p.bin && !(p.rr > 0.0)) return fail(DTB_E_INVALID, "r: must be > 0, got %g", p.rr);
     const int rad = win / 2;
     const size_t smem = gs_smem_bytes(rad);
     if (smem > DTB_GS_MAX_SMEM)

@@ -119,3 +119,12 @@ def test_gen_synthetic_matches_reference_pages():
         memory_model("fast", 10)
     with pytest.raises(ValueError, match="too small"):
         gen_synthetic(SyntheticSpec(width=8))
+
+
+def test_to_gray_refuses_non_byte_channels_without_a_gpu_call():
+    import numpy as np
+    from paper_1210_3165_b200 import to_gray
+    with pytest.raises(ValueError, match="to_gray"):
+        to_gray(np.full((2, 2, 3), 300, dtype=np.int32))
+    with pytest.raises(ValueError, match="to_gray"):
+        to_gray(np.full((2, 2, 3), 0.5))
