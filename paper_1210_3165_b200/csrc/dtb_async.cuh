@@ -76,6 +76,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         " [%0], [%1], %2, [%3], %4;"
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
 }
+// 3-D tiled tensor copy (tensor map in param space): box {x, y, z} of the map -> dst, bytes
+// outside the tensor are zero-filled; completion on the mbarrier's tx count (full box bytes).
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z, uint64_t* bar,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+        ::"r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
 // L2 eviction priorities: a row is read three times (entering, centre r steps later, leaving
 // 2r+1 steps later); keep it resident on the first two reads, let it go on the last.
 __device__ __forceinline__ uint64_t make_policy(int kind) {

@@ -1104,7 +1104,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     {
         const int bbm = bb_mode();
         const long long px = (long long)p.cols * (p.out_end - p.out_begin) * n_images;
-        if (bbm && !p.tmap && bb_eligible(p) &&
+        if (bbm && !p.tmap && bb_eligible(p) && bb_tma_ok(p, n_images) &&
             (bbm == 1 || p.r >= DTB_BB_MIN_R || (p.r >= DTB_BB_MIN_R_LARGE && px >= (1ll << 26))))
             return launch_block(p, n_images, num_sms, st, print_plan());
     }

@@ -73,6 +73,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
 
 // Block-sum group-bound Sauvola kernel (dtb_block.cu): eligibility and launcher.
 bool bb_eligible(const SlideParams& p);
+bool bb_tma_ok(const SlideParams& p, int n_images);  // tensor-map staging prerequisites
 cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t st, bool print);
 cudaError_t set_fp32_audit_block(unsigned long long* counters);
 cudaError_t bb_exact_count(unsigned long long* out, bool reset);
