@@ -60,15 +60,6 @@ namespace dtb {
 #ifndef BB_STAGES
 #define BB_STAGES 3  // ring depth per warp (the warp refills a slot right after consuming it)
 #endif
-#ifndef BB_POL_F
-#define BB_POL_F 2     // L2 policy of the centre-row copy (2 evict_last, 1 evict_first, 0 normal)
-#endif
-#ifndef BB_POL_WARM
-#define BB_POL_WARM 2  // warm-up rows above the band: 2 evict_last, 1 evict_first
-#endif
-#ifndef BB_POL_E
-#define BB_POL_E 2
-#endif
 #ifndef BB_GPL
 #define BB_GPL (BB_NC_DEF / 256)  // group slots per lane (groups of 8 output columns)
 #endif
@@ -312,6 +303,25 @@ __device__ __forceinline__ bool bb_elect() {
     return e != 0;
 }
 
+// The two warps' halves of the shared warm-up: each publishes its partial block sums, waits for
+// the partner (named barrier 1, both warps), and adds the partner's half.
+__device__ __forceinline__ void bb_exchange(uint32_t* xbuf, int warp, int lane, uint32_t (&bS)[BB_BPL],
+                                            uint32_t (&bQ)[BB_BPL]) {
+    uint32_t* mine = xbuf + warp * (2 * BB_BPL * 32);
+    const uint32_t* other = xbuf + (warp ^ 1) * (2 * BB_BPL * 32);
+#pragma unroll
+    for (int j = 0; j < BB_BPL; ++j) {
+        mine[j * 32 + lane] = bS[j];
+        mine[(BB_BPL + j) * 32 + lane] = bQ[j];
+    }
+    __syncthreads();  // the CTA is exactly the two warps
+#pragma unroll
+    for (int j = 0; j < BB_BPL; ++j) {
+        bS[j] += other[j * 32 + lane];
+        bQ[j] += other[(BB_BPL + j) * 32 + lane];
+    }
+}
+
 // CUtensorMap storage (128 bytes, 64-byte aligned) as a kernel parameter; one map per input
 // segment (map 0 = the single buffer)
 struct alignas(64) BBTensorMap {
@@ -321,26 +331,32 @@ struct BBMaps {
     BBTensorMap m[3];
 };
 
-// One CTA = one warp = one pipeline: a strip of BB_NC staged columns x a band of output rows of
-// one image.  blockIdx.x -> (strip, band, image), strips fastest.  Every control value is
-// warp-uniform; lane 0 (elected) issues the bulk copies.
+// One CTA = two warps = two pipelines over the same strip: band 2j+1 (warp 0, top to bottom)
+// and band 2j (warp 1, bottom to top).  Both start at their common boundary row B, so their
+// initial window sums are the same 2r+1 rows (up to one row): the warps split those warm-up rows,
+// add their partial block sums through shared memory, and each then runs its own band.  This
+// halves the warm-up reads and work (the warm-up is ~12% of the C4 page and ~45% of a 2048-row
+// band).  blockIdx.x -> (strip, band pair, image), strips fastest.  Control values are warp-
+// uniform; one elected lane per warp issues its tensor-map copies.
 template <bool SEG, int MINB>
-__global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ SlideParams p,
+__global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ SlideParams p,
                                                       const __grid_constant__ BBMaps mp,
-                                                      int nstrips, int nbands, int tw0) {
+                                                      int nstrips, int npairs, int tw0, int paired) {
     constexpr int NS = BB_STAGES, NC = BB_NC, NB = BB_NB, PLW = BB_PLW;
     extern __shared__ __align__(128) uint8_t smb[];
-    uint8_t* ring = smb;
-    uint32_t* PSe = reinterpret_cast<uint32_t*>(smb + NS * 3 * NC);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    uint8_t* ring = smb + warp * BB_WARP_BYTES;
+    uint32_t* PSe = reinterpret_cast<uint32_t*>(ring + NS * 3 * NC);
     uint32_t* PQe = PSe + 2 * PLW;
     uint64_t* full = reinterpret_cast<uint64_t*>(PSe + 4 * PLW);
-    const int lane = threadIdx.x;
-    const int pid = blockIdx.x;
+    uint32_t* xbuf = reinterpret_cast<uint32_t*>(smb + 2 * BB_WARP_BYTES);  // [warp][2 BPL][32]
+    const int pid = 2 * (int)blockIdx.x + warp;  // pipeline id (debug timeline)
     unsigned long long* const tdbg = (g_bb_times && pid < g_bb_times_cap) ? g_bb_times + 4 * pid : nullptr;
     if (tdbg && lane == 0) { tdbg[2] = 0; tdbg[3] = 0; }
     if (tdbg && lane == 0) tdbg[0] = bb_gtimer();
-    const int strip = pid % nstrips, rest = pid / nstrips;
-    const int band = rest % nbands, img = rest / nbands;
+    const int strip = (int)blockIdx.x % nstrips, rest = (int)blockIdx.x / nstrips;
+    const int pair = rest % npairs, img = rest / npairs;
     const int r = p.r;
     const int alpha = (16 - (r & 15)) & 15;
     // strip widths: the first strip tw0 (narrower: its edge groups cost per-pixel bounds), the
@@ -348,14 +364,26 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
     const int X0 = strip == 0 ? 0 : tw0 + (strip - 1) * p.TW;
     const int TWs = strip == 0 ? tw0 : p.TW;
     const int xc0 = X0 - r - alpha;
-    const int ya = p.out_begin + band * p.TH;
-    const int yb = min(ya + p.TH, p.out_end);
-    if (ya >= yb) return;
+    // B = first row of band 2j+1 (or the end of the output rows); warp 0 outputs [B, yb) going
+    // down, warp 1 outputs [ya, B) going up
+    const int ya_up = p.out_begin + 2 * pair * p.TH;
+    const int B = min(ya_up + p.TH, p.out_end);
+    // paired == 0 (tall bands, where the warm-up is a small share): both warps run downward
+    // bands with their own warm-ups (band 2j from ya_up, band 2j+1 from B)
+    const bool pr = paired != 0;
+    const int d = (warp == 0 || !pr) ? 1 : -1;
+    const int ystart = warp == 0 ? B : (pr ? B - 1 : ya_up);
+    const int nmain = warp == 0 ? max(min(B + p.TH, p.out_end) - B, 0) : B - ya_up;
     const uint8_t* in0 = p.in + (int64_t)img * p.img_stride - (int64_t)p.row0 * p.pitch;
-    const int g0 = max(ya - r, 0);
-    const int nwr = min(ya + r, p.H - 1) - g0 + 1;  // warm-up rows (3 per item)
-    const int nwarm = (nwr + 2) / 3;
-    const int n_items = nwarm + (yb - ya);
+    // warm-up window [Bw - r, Bw + r] (clipped), items of 3 rows; paired: the shared window at B,
+    // warp 0 takes the first half of the items, warp 1 the rest
+    const int Bw = (pr || warp == 0) ? B : ya_up;
+    const int g0 = max(Bw - r, 0);
+    const int nwr = min(Bw + r, p.H - 1) - g0 + 1;
+    const int nw_all = (nwr + 2) / 3, nw_half = pr ? (nw_all + 1) / 2 : nw_all;
+    const int wlo = (warp == 0 || !pr) ? 0 : nw_half;
+    const int nwarm = warp == 0 ? nw_half : (pr ? nw_all - nw_half : nw_all);
+    const int n_items = nwarm + nmain;
 
     // (tensor-map copies zero-fill every column / row outside the image: each copy writes its
     // whole ring slot, no ring initialisation)
@@ -365,15 +393,15 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
     }
     __syncwarp();
 
-    const uint64_t pol_keep = make_policy(BB_POL_E), pol_drop = make_policy(1), pol_f = make_policy(BB_POL_F);
-    const uint64_t pol_warm = make_policy(BB_POL_WARM);
+    const uint64_t pol_keep = make_policy(2), pol_drop = make_policy(1);
     const int x8E = xc0 >> 3, x8F = X0 >> 3;  // tensor-map column coordinates (8-byte elements)
     // ragged width (cols % 8): the map covers whole 8-byte elements; the consumer patches the last
     // cols % 8 bytes of each staged row in from global memory
     const int cols8 = p.cols & ~7;
     const bool rag = cols8 < p.cols && xc0 + NC > cols8;
-    // item k -> ring slot k % NS: warm-up items carry rows g0+3k.. in the E, O, F slots; row
-    // items the entering row y+r (E), leaving row y-r-1 (O) and centre row y (F, output columns)
+    // item k -> ring slot k % NS: warm-up items carry rows g0+3(wlo+k).. in the E, O, F slots;
+    // row items the entering row y+dr (E), leaving row y-d(r+1) (O) and centre row y (F, output
+    // columns).  The downward band's first row is already covered by the warm-up (only F).
 
     // ---- output-side constants
     const int iL = (alpha + 10) >> 2, iH = (alpha + 2 * r + 1) >> 2;   // I' = [2g+iL, 2g+iH)
@@ -430,19 +458,19 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
             if (bb_elect()) {
                 if (rag) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tail patches
                 if (kk < nwarm) {
-                    const int g = g0 + 3 * kk, cnt = min(3, g0 + nwr - g);
+                    const int g = g0 + 3 * (wlo + kk), cnt = min(3, g0 + nwr - g);
                     mbar_expect_tx(&full[s], (uint32_t)cnt * NC);
-                    for (int i = 0; i < cnt; ++i) stage_row(E + i * NC, x8E, g + i, g + i < ya ? pol_warm : pol_keep);
+                    for (int i = 0; i < cnt; ++i) stage_row(E + i * NC, x8E, g + i, pol_keep);
                 } else {
-                    const int y = ya + (kk - nwarm);
-                    if (kk == nwarm) {
+                    const int y = ystart + d * (kk - nwarm);
+                    if (kk == nwarm && d > 0) {
                         mbar_expect_tx(&full[s], NC);
                     } else {
                         mbar_expect_tx(&full[s], 3 * NC);
-                        stage_row(E, x8E, y + r, pol_keep);
-                        stage_row(E + NC, x8E, y - r - 1, pol_drop);
+                        stage_row(E, x8E, y + d * r, pol_keep);
+                        stage_row(E + NC, x8E, y - d * (r + 1), pol_drop);
                     }
-                    stage_row(E + 2 * NC, x8F, y, pol_f);
+                    stage_row(E + 2 * NC, x8F, y, pol_keep);
                 }
             }
         }
@@ -457,13 +485,14 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
                 const int w = lane >> 3, b = lane & 7;
                 int g = -1, off = cols8 - xc0;
                 if (k < nwarm) {
-                    const int g1 = g0 + 3 * k + w;
+                    const int g1 = g0 + 3 * (wlo + k) + w;
                     if (g1 < g0 + nwr) g = g1;
                 } else {
-                    const int y = ya + (k - nwarm);
-                    const bool fst = k == nwarm;
-                    if (w == 0 && !fst && y + r < p.H) g = y + r;
-                    if (w == 1 && !fst && y - r - 1 >= 0) g = y - r - 1;
+                    const int y = ystart + d * (k - nwarm);
+                    const bool fst = k == nwarm && d > 0;
+                    if (w == 0 && !fst) g = y + d * r;
+                    if (w == 1 && !fst) g = y - d * (r + 1);
+                    if (g >= p.H) g = -1;
                     if (w == 2) { g = y; off = cols8 - X0; }
                 }
                 if (g >= 0 && b < nt && off + b >= 0 && off + b < NC) st[w * NC + off + b] = row_at<SEG>(p, in0, g)[cols8 + b];
@@ -472,7 +501,7 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
         }
         const uint8_t* stage = ring + s * 3 * NC;
         if (k < nwarm) {
-            const int cnt = min(3, nwr - 3 * k);
+            const int cnt = min(3, nwr - 3 * (wlo + k));
             for (int i = 0; i < cnt; ++i) {
                 const uint4* R = reinterpret_cast<const uint4*>(stage + i * NC + 4 * BB_BPL * lane);
 #pragma unroll
@@ -487,9 +516,12 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
                 }
             }
         } else {
-            const int y = ya + (k - nwarm);
-            const bool fst = (k == nwarm);
-            if (tdbg && fst && lane == 0) tdbg[3] = bb_gtimer();
+            const int y = ystart + d * (k - nwarm);
+            const bool fst = k == nwarm && d > 0;
+            if (k == nwarm) {
+                if (pr) bb_exchange(xbuf, warp, lane, bS, bQ);
+                if (tdbg && lane == 0) tdbg[3] = bb_gtimer();
+            }
             // ---- column side: block sums, exclusive block prefix -> even / odd planes
             if (!fst) {
                 const uint4* E = reinterpret_cast<const uint4*>(stage + 4 * BB_BPL * lane);
@@ -655,6 +687,7 @@ __global__ void __launch_bounds__(32, MINB) bb_kernel(const __grid_constant__ Sl
         }
         __syncwarp();  // every lane is done with slot s (and, for a row, with the prefix)
     }
+    if (pr && nmain == 0) bb_exchange(xbuf, warp, lane, bS, bQ);  // the partner still needs our half
     if (tdbg && lane == 0) tdbg[1] = bb_gtimer();
 }
 
@@ -748,17 +781,20 @@ bool bb_eligible(const SlideParams& p) {
 
 struct BBCache {
     std::mutex mu;
-    int occ[64][2];          // [device][seg] CTAs (= pipelines) per SM (0 = unknown)
+    int occ[64][2];          // [device][seg] CTAs (pipeline pairs) per SM (0 = unknown)
     bool smem_set[64][2];    // dynamic-smem opt-in raised
 };
 static BBCache g_bb;
+
+// dynamic shared memory per CTA: two warps' rings / prefix planes / mbarriers + the exchange
+constexpr int BB_CTA_BYTES = 2 * BB_WARP_BYTES + 2 * 2 * BB_BPL * 32 * 4;
 
 template <bool SEG, int MINB>
 static cudaError_t bb_prepare(int dev, int* occ) {
     std::lock_guard<std::mutex> lk(g_bb.mu);
     if (dev < 0 || dev >= 64) return cudaErrorInvalidValue;
     auto fn = bb_kernel<SEG, MINB>;
-    const size_t smem = BB_WARP_BYTES;
+    const size_t smem = BB_CTA_BYTES;
     if (!g_bb.smem_set[dev][SEG]) {
         const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -766,7 +802,7 @@ static cudaError_t bb_prepare(int dev, int* occ) {
     }
     int& o = g_bb.occ[dev][SEG];
     if (!o) {
-        const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32, smem);
+        const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 64, smem);
         if (e != cudaSuccess) return e;
         if (o < 1) o = 1;
     }
@@ -774,21 +810,22 @@ static cudaError_t bb_prepare(int dev, int* occ) {
     return cudaSuccess;
 }
 
-// Band count: the cost per pipeline slot is waves x (TH + wf (2r+1)) + tf TH in main-row units
-// (a warm-up row is two dp4a per 4 columns, ~1/10 of a main row; tf stands for the content-
-// dependent spread of band cost).
-static int bb_plan_bands(int rows_out, int units, int slots, int r) {
-    const double wf = 0.1, tf = 0.1;
+// Band-pair count: the cost per CTA slot is waves x (TH + wf (2r+1) / (paired ? 2 : 1)) + tf TH
+// in main-row units (a warm-up row is two dp4a per 4 columns, ~1/10 of a main row, and each
+// pipeline of a pair stages half of the shared warm-up; tf stands for the content-dependent
+// spread of band cost).  units = strips x images, slots = CTAs (pairs) resident at once.
+static int bb_plan_pairs(int rows_out, int units, int slots, int r, bool paired) {
+    const double wf = paired ? 0.05 : 0.1, tf = 0.1;
     int best = 1;
     double best_cost = 1e300;
-    const int nb_max = std::max(1, std::min((rows_out + 7) / 8, 4 * slots / std::max(1, units) + 1));
-    for (int nb = 1; nb <= nb_max; ++nb) {
-        const int th = (rows_out + nb - 1) / nb;
-        const int waves = (units * nb + slots - 1) / slots;
+    const int np_max = std::max(1, std::min((rows_out + 15) / 16, 4 * slots / std::max(1, units) + 1));
+    for (int np = 1; np <= np_max; ++np) {
+        const int th = (rows_out + 2 * np - 1) / (2 * np);
+        const int waves = (units * np + slots - 1) / slots;
         const double cost = waves * (th + wf * (2 * r + 1)) + tf * th;
-        if (cost < best_cost) { best_cost = cost; best = nb; }
+        if (cost < best_cost) { best_cost = cost; best = np; }
     }
-    return std::max(1, std::min(best, (rows_out + 7) / 8));
+    return best;
 }
 
 cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t st, bool print) {
@@ -820,25 +857,34 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     int occ = 1;
-    e = p.nseg ? bb_prepare<true, 16>(dev, &occ) : bb_prepare<false, 16>(dev, &occ);
+    e = p.nseg ? bb_prepare<true, 8>(dev, &occ) : bb_prepare<false, 8>(dev, &occ);
     if (e != cudaSuccess) return e;
     const int rows_out = p.out_end - p.out_begin;
-    const int nbands = bb_plan_bands(rows_out, ns * n_images, num_sms * occ, p.r);
-    p.TH = (rows_out + nbands - 1) / nbands;
-    const int nb = (rows_out + p.TH - 1) / p.TH;
-    const long long np = (long long)ns * nb * n_images;
-    if (np > 0x7fffffffll) return cudaErrorInvalidValue;
-    const int ctas = (int)np;
-    const size_t smem = BB_WARP_BYTES;
+    // Pair the bands (shared warm-up, one band running upward) when the bands come out shorter
+    // than the window: 2048-row C4 band 0.080 -> 0.066 ms; on the whole C4 page (TH 139 > W)
+    // pairing measured 1.5% slower (0.343 vs 0.337 ms), so tall bands keep separate warm-ups.
+    bool paired = true;
+    int npairs0 = bb_plan_pairs(rows_out, ns * n_images, num_sms * occ, p.r, true);
+    if ((rows_out + 2 * npairs0 - 1) / (2 * npairs0) >= 2 * p.r + 1) {
+        paired = false;
+        npairs0 = bb_plan_pairs(rows_out, ns * n_images, num_sms * occ, p.r, false);
+    }
+    p.TH = (rows_out + 2 * npairs0 - 1) / (2 * npairs0);
+    const int nb = (rows_out + p.TH - 1) / p.TH;  // non-empty bands; pair j = bands 2j, 2j+1
+    const int npairs = (nb + 1) / 2;
+    const long long nc = (long long)ns * npairs * n_images;
+    if (nc > 0x7fffffffll) return cudaErrorInvalidValue;
+    const int ctas = (int)nc;
+    const size_t smem = BB_CTA_BYTES;
     if (print)
-        fprintf(stderr, "[dtb plan] bb_kernel cols=%d rows=%d r=%d strips=%d TW=%d (first %d) bands=%d TH=%d pipes=%lld ctas=%d occ=%d smem=%zu\n",
-                p.cols, rows_out, p.r, ns, p.TW, tw0, nb, p.TH, np, ctas, occ, smem);
+        fprintf(stderr, "[dtb plan] bb_kernel cols=%d rows=%d r=%d strips=%d TW=%d (first %d) bands=%d TH=%d pairs=%d%s ctas=%d occ=%d smem=%zu\n",
+                p.cols, rows_out, p.r, ns, p.TW, tw0, nb, p.TH, npairs, paired ? " (shared warm-up)" : "", ctas, occ, smem);
     BBMaps mp{};
     e = bb_encode_maps(p, n_images, &mp);
     if (e != cudaSuccess) return e;
     set_last_kernel("bb_kernel");
-    if (p.nseg) bb_kernel<true, 16><<<ctas, 32, smem, st>>>(p, mp, ns, nb, tw0);
-    else bb_kernel<false, 16><<<ctas, 32, smem, st>>>(p, mp, ns, nb, tw0);
+    if (p.nseg) bb_kernel<true, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0);
+    else bb_kernel<false, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0);
     return cudaGetLastError();
 }
 

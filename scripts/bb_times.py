@@ -57,7 +57,7 @@ print(mode, "ctas", n, "span us %.1f" % en.max(), "start max %.1f" % st.max())
 for name, v in (("duration", dur), ("warm-up", warm), ("main", en - wu)):
     print("%-9s us: min %.1f p50 %.1f p90 %.1f max %.1f" % (name, v.min(), np.median(v), np.percentile(v, 90), v.max()))
 ns = int(sys.argv[3]) if len(sys.argv) > 3 else 20
-strip = np.arange(n) % ns
+strip = (np.arange(n) // 2) % ns  # pipelines 2c, 2c+1 share CTA c
 for s_ in range(ns):
     m = strip == s_
     print("strip %2d dur mean %.1f max %.1f  warm mean %.1f  exact %d" % (s_, dur[m].mean(), dur[m].max(), warm[m].mean(), t[m, 2].sum()))

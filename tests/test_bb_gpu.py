@@ -170,8 +170,8 @@ def test_random_pages_and_params(seed):
 
 @pytest.mark.parametrize("w", [130, 1003, 2550, 4097])
 def test_odd_widths_pitched(w):
-    # widths that are not a multiple of 16 arrive in a 16-byte pitched buffer: the tensor-map
-    # staging reads the padding bytes of the last chunk, which the kernel must mask
+    # widths that are not a multiple of 16 arrive in a 16-byte pitched buffer: the tensor map
+    # covers whole 8-byte chunks, the kernel patches the last cols % 8 bytes of each staged row
     img = workloads.doc_gray(170, w, w, 90)
     _check(img, 2 * min(63, (w - 1) // 2) + 1, 0.34)
 
@@ -189,3 +189,19 @@ def test_odd_width_band_and_segments():
     out = engine.binarize_segments(segs, 0, 600, 0, 600, 101, "sauvola", 0.34, 128.0)
     assert _ran_bb()
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("h", [17, 63, 64, 65, 129, 131, 200, 257, 1030])
+def test_band_pair_counts(h):
+    # pipelines run in pairs sharing one warm-up (one band downward, one upward from their
+    # common row); heights give odd / even band counts and a pair whose downward band is empty
+    img = workloads.doc_gray(h, 1500, 3 + h % 11, 1300)
+    _check(img, 63, 0.34)
+
+
+def test_tall_bands_unpaired_and_short_bands_paired():
+    # a tall page plans bands taller than W (separate warm-ups), a short one shorter (shared);
+    # both parities against the oracle
+    for h, w in ((1400, 41), (300, 201)):
+        img = workloads.doc_gray(h, 3000, 5, 1400 + h)
+        _check(img, w, 0.34)
