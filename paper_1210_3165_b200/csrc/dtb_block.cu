@@ -297,6 +297,20 @@ __device__ __forceinline__ bool bb_pixel_refine(const uint32_t* PS, const uint32
     return open;
 }
 
+// Opaque copies: the value must live in a register from here on (ptxas cannot re-derive it).
+__device__ __forceinline__ int bb_pin(int v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
+__device__ __forceinline__ uint32_t bb_pin(uint32_t v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
+__device__ __forceinline__ float bb_pinf(float v) {
+    asm volatile("" : "+f"(v));
+    return v;
+}
+
 __device__ __forceinline__ bool bb_elect() {
     uint32_t e;
     asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n}" : "=r"(e));
@@ -344,7 +358,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
                                                       int nstrips, int npairs, int tw0, int paired) {
     constexpr int NS = BB_STAGES, NC = BB_NC, NB = BB_NB, PLW = BB_PLW;
     extern __shared__ __align__(128) uint8_t smb[];
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform for the compiler
     const int lane = threadIdx.x & 31;
     uint8_t* ring = smb + warp * BB_WARP_BYTES;
     uint32_t* PSe = reinterpret_cast<uint32_t*>(ring + NS * 3 * NC);
@@ -393,7 +407,21 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
     }
     __syncwarp();
 
-    const uint64_t pol_keep = make_policy(2), pol_drop = make_policy(1);
+    // L2 priorities of the three reads of a row (BB_POL_*: 0 normal, 1 evict-first, 2 evict-last).
+    // With bands about as tall as the window, the leaving row of band j+1 is the entering row of
+    // band j a few steps later (and the other way round for bands shorter than the window), so
+    // the leaving row stays; measured on C4 (ncu dram__bytes_read): E/O/F = last/first/last 1050 MB,
+    // last/last/first 886 MB, first/last/first 846 MB, all normal 925 MB (kernel time within 2%).
+#ifndef BB_POL_E
+#define BB_POL_E 1
+#endif
+#ifndef BB_POL_O
+#define BB_POL_O 2
+#endif
+#ifndef BB_POL_F
+#define BB_POL_F 1
+#endif
+    const uint64_t pol_E = make_policy(BB_POL_E), pol_O = make_policy(BB_POL_O), pol_F = make_policy(BB_POL_F);
     const int x8E = xc0 >> 3, x8F = X0 >> 3;  // tensor-map column coordinates (8-byte elements)
     // ragged width (cols % 8): the map covers whole 8-byte elements; the consumer patches the last
     // cols % 8 bytes of each staged row in from global memory
@@ -403,19 +431,23 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
     // row items the entering row y+dr (E), leaving row y-d(r+1) (O) and centre row y (F, output
     // columns).  The downward band's first row is already covered by the warm-up (only F).
 
-    // ---- output-side constants
+    // ---- output-side constants.  The values the row loop reads every iteration are pinned in
+    // registers (bb_pin): at 128 registers ptxas otherwise re-derives them from the kernel
+    // parameters in every row (~85 instructions per row in the round-2 profile).
     const int iL = (alpha + 10) >> 2, iH = (alpha + 2 * r + 1) >> 2;   // I' = [2g+iL, 2g+iH)
     const int uL = alpha >> 2, uH = (alpha + 2 * r + 11) >> 2;         // U' = [2g+uL, 2g+uH)
     // per-stream prefix pointers for this lane's first group (g = lane); slot i adds 32 words
-    const uint32_t* pSiH = PSe + (iH & 1) * PLW + (iH >> 1) + lane;
-    const uint32_t* pSiL = PSe + (iL & 1) * PLW + (iL >> 1) + lane;
-    const uint32_t* pSuH = PSe + (uH & 1) * PLW + (uH >> 1) + lane;
-    const uint32_t* pSuL = PSe + (uL & 1) * PLW + (uL >> 1) + lane;
+    const uint32_t* pSiH = PSe + bb_pin((iH & 1) * PLW + (iH >> 1) + lane);
+    const uint32_t* pSiL = PSe + bb_pin((iL & 1) * PLW + (iL >> 1) + lane);
+    const uint32_t* pSuH = PSe + bb_pin((uH & 1) * PLW + (uH >> 1) + lane);
+    const uint32_t* pSuL = PSe + bb_pin((uL & 1) * PLW + (uL >> 1) + lane);
     const int W = 2 * r + 1;
     const uint32_t nUc = 4u * (uint32_t)(uH - uL), nIc = 4u * (uint32_t)(iH - iL);
     const float kUp = 1.0f + 7.62939453125e-6f, kDn = 1.0f - 7.62939453125e-6f;  // 1 +- 2^-17
-    const float a_up = p.a * kUp, a_dn = p.a * kDn, cK_up = p.c * kUp, cK_dn = p.c * kDn, tol = p.tol;
-    const bool vec_ok = (((uintptr_t)p.bin | (uintptr_t)p.bin_pitch | (uintptr_t)p.out_stride) & 7) == 0;
+    const float a_up = bb_pinf(p.a * kUp), a_dn = bb_pinf(p.a * kDn), cK_up = bb_pinf(p.c * kUp);
+    const float cK_dn = p.c * kDn, tol = p.tol;
+    const bool vec_ok =
+        bb_pin((int)((((uintptr_t)p.bin | (uintptr_t)p.bin_pitch | (uintptr_t)p.out_stride) & 7) == 0)) != 0;
     // group slots of this lane: imask = interior groups (all 8 windows inside the image in x)
     uint32_t imask = 0;
     // (uniform) valid groups ngv; left-edge groups [0, gl), right-edge groups [gr, ngv)
@@ -431,263 +463,323 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             if (x0 - r >= 0 && x0 + 7 + r <= p.cols - 1) imask |= 1u << i;
         }
     }
+    imask = bb_pin(imask);
     uint8_t* obase = p.bin + (int64_t)img * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
     const float rnW = 1.0f / (float)(W * W);  // interior rows: n = W^2
 
     uint32_t bS[BB_BPL], bQ[BB_BPL];
 #pragma unroll
     for (int j = 0; j < BB_BPL; ++j) { bS[j] = 0; bQ[j] = 0; }
-    // one issue site: iteration k first refills the slot item k-1 left (item k+NS-1), then
-    // consumes item k; the first NS-1 iterations only fill the ring
-    for (int k = 1 - NS; k < n_items; ++k) {
-        BB_PERTURB(pid, 4 * k);
-        if (k + NS - 1 < n_items) {
-            // box = one row of NC bytes (128 8-byte elements) at (x8, row, image); segmented input:
-            // the map of the segment holding the row (rows outside the image read as zeros)
-            const int kk = k + NS - 1;
-            const int s = kk % NS;
-            uint8_t* E = ring + s * 3 * NC;
-            auto stage_row = [&](uint8_t* dst, int x8, int g, uint64_t pol) {
-                if (SEG) {
-                    const int i = g >= p.seg_lo[2] ? 2 : (g >= p.seg_lo[1] ? 1 : 0);
-                    tma_load_3d(dst, &mp.m[i], x8, g - p.seg_lo[i], 0, &full[s], pol);
-                } else {
-                    tma_load_3d(dst, &mp.m[0], x8, g - p.row0, img, &full[s], pol);
-                }
-            };
-            if (bb_elect()) {
-                if (rag) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tail patches
-                if (kk < nwarm) {
-                    const int g = g0 + 3 * (wlo + kk), cnt = min(3, g0 + nwr - g);
-                    mbar_expect_tx(&full[s], (uint32_t)cnt * NC);
-                    for (int i = 0; i < cnt; ++i) stage_row(E + i * NC, x8E, g + i, pol_keep);
-                } else {
-                    const int y = ystart + d * (kk - nwarm);
-                    if (kk == nwarm && d > 0) {
-                        mbar_expect_tx(&full[s], NC);
-                    } else {
-                        mbar_expect_tx(&full[s], 3 * NC);
-                        stage_row(E, x8E, y + d * r, pol_keep);
-                        stage_row(E + NC, x8E, y - d * (r + 1), pol_drop);
-                    }
-                    stage_row(E + 2 * NC, x8F, y, pol_keep);
-                }
-            }
-        }
-        if (k < 0) continue;
-        const int s = k % NS;
-        mbar_wait(&full[s], (k / NS) & 1);
-        BB_PERTURB(pid, 4 * k + 1);
-        if (rag) {  // bytes [cols8, cols) of the rows this item staged (rows outside stay zero)
-            uint8_t* st = ring + s * 3 * NC;
-            const int nt = p.cols - cols8;
-            if (lane < 3 * 8) {
-                const int w = lane >> 3, b = lane & 7;
-                int g = -1, off = cols8 - xc0;
-                if (k < nwarm) {
-                    const int g1 = g0 + 3 * (wlo + k) + w;
-                    if (g1 < g0 + nwr) g = g1;
-                } else {
-                    const int y = ystart + d * (k - nwarm);
-                    const bool fst = k == nwarm && d > 0;
-                    if (w == 0 && !fst) g = y + d * r;
-                    if (w == 1 && !fst) g = y - d * (r + 1);
-                    if (g >= p.H) g = -1;
-                    if (w == 2) { g = y; off = cols8 - X0; }
-                }
-                if (g >= 0 && b < nt && off + b >= 0 && off + b < NC) st[w * NC + off + b] = row_at<SEG>(p, in0, g)[cols8 + b];
-            }
-            __syncwarp();
-        }
-        const uint8_t* stage = ring + s * 3 * NC;
-        if (k < nwarm) {
-            const int cnt = min(3, nwr - 3 * (wlo + k));
-            for (int i = 0; i < cnt; ++i) {
-                const uint4* R = reinterpret_cast<const uint4*>(stage + i * NC + 4 * BB_BPL * lane);
-#pragma unroll
-                for (int h = 0; h < BB_BPL / 4; ++h) {
-                    const uint4 a = R[h];
-                    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        bS[4 * h + j] = __dp4a(w[j], 0x01010101u, bS[4 * h + j]);
-                        bQ[4 * h + j] = __dp4a(w[j], w[j], bQ[4 * h + j]);
-                    }
-                }
-            }
+
+    // box = one row of NC bytes (128 8-byte elements) at (x8, row, image); segmented input: the
+    // map of the segment holding the row (rows outside the image read as zeros)
+    auto stage_row = [&](uint8_t* dst, int x8, int g, uint64_t* bar, uint64_t pol) {
+        if (SEG) {
+            const int i = g >= p.seg_lo[2] ? 2 : (g >= p.seg_lo[1] ? 1 : 0);
+            tma_load_3d(dst, &mp.m[i], x8, g - p.seg_lo[i], 0, bar, pol);
         } else {
-            const int y = ystart + d * (k - nwarm);
-            const bool fst = k == nwarm && d > 0;
-            if (k == nwarm) {
-                if (pr) bb_exchange(xbuf, warp, lane, bS, bQ);
-                if (tdbg && lane == 0) tdbg[3] = bb_gtimer();
+            tma_load_3d(dst, &mp.m[0], x8, g - p.row0, img, bar, pol);
+        }
+    };
+    // item kk (warm-up or row) into ring slot sl, by one elected lane
+    auto issue = [&](int kk, int sl) {
+        BB_PERTURB(pid, 4 * kk);
+        uint8_t* E = ring + sl * 3 * NC;
+        if (bb_elect()) {
+            if (rag) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tail patches
+            if (kk < nwarm) {
+                const int g = g0 + 3 * (wlo + kk), cnt = min(3, g0 + nwr - g);
+                mbar_expect_tx(&full[sl], (uint32_t)cnt * NC);
+                for (int i = 0; i < cnt; ++i) stage_row(E + i * NC, x8E, g + i, &full[sl], pol_E);
+            } else {
+                const int y = ystart + d * (kk - nwarm);
+                if (kk == nwarm && d > 0) {
+                    mbar_expect_tx(&full[sl], NC);
+                } else {
+                    mbar_expect_tx(&full[sl], 3 * NC);
+                    stage_row(E, x8E, y + d * r, &full[sl], pol_E);
+                    stage_row(E + NC, x8E, y - d * (r + 1), &full[sl], pol_O);
+                }
+                stage_row(E + 2 * NC, x8F, y, &full[sl], pol_F);
             }
-            // ---- column side: block sums, exclusive block prefix -> even / odd planes
-            if (!fst) {
-                const uint4* E = reinterpret_cast<const uint4*>(stage + 4 * BB_BPL * lane);
-                const uint4* O = reinterpret_cast<const uint4*>(stage + NC + 4 * BB_BPL * lane);
+        }
+    };
+    // ragged width: bytes [cols8, cols) of the rows item k staged in slot sl (rows outside stay zero)
+    auto rag_patch = [&](int k, int sl) {
+        uint8_t* st = ring + sl * 3 * NC;
+        const int nt = p.cols - cols8;
+        if (lane < 3 * 8) {
+            const int w = lane >> 3, b = lane & 7;
+            int g = -1, off = cols8 - xc0;
+            if (k < nwarm) {
+                const int g1 = g0 + 3 * (wlo + k) + w;
+                if (g1 < g0 + nwr) g = g1;
+            } else {
+                const int y = ystart + d * (k - nwarm);
+                const bool fst = k == nwarm && d > 0;
+                if (w == 0 && !fst) g = y + d * r;
+                if (w == 1 && !fst) g = y - d * (r + 1);
+                if (g >= p.H) g = -1;
+                if (w == 2) { g = y; off = cols8 - X0; }
+            }
+            if (g >= 0 && b < nt && off + b >= 0 && off + b < NC) st[w * NC + off + b] = row_at<SEG>(p, in0, g)[cols8 + b];
+        }
+        __syncwarp();
+    };
+
+    // ---- ring fill, then the warm-up items (block sums of the initial window).  cs / cph: the
+    // consumer's slot and phase parity; ps: the slot the previous item left, refilled with item
+    // k + NS - 1 at the top of iteration k.
+    int cs = 0, ps = NS - 1;
+    uint32_t cph = 0;
+    for (int kk = 0; kk < NS - 1 && kk < n_items; ++kk) issue(kk, kk);
+    for (int k = 0; k < nwarm; ++k) {
+        if (k + NS - 1 < n_items) issue(k + NS - 1, ps);
+        mbar_wait(&full[cs], cph);
+        BB_PERTURB(pid, 4 * k + 1);
+        if (rag) rag_patch(k, cs);
+        const uint8_t* stage = ring + cs * 3 * NC;
+        const int cnt = min(3, nwr - 3 * (wlo + k));
+        for (int i = 0; i < cnt; ++i) {
+            const uint4* R = reinterpret_cast<const uint4*>(stage + i * NC + 4 * BB_BPL * lane);
 #pragma unroll
-                for (int h = 0; h < BB_BPL / 4; ++h) {
-                    const uint4 ev = E[h], ov = O[h];  // rows outside the image: zeros
-                    const uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
-                    const uint32_t o[4] = {ov.x, ov.y, ov.z, ov.w};
+            for (int h = 0; h < BB_BPL / 4; ++h) {
+                const uint4 a = R[h];
+                const uint32_t w[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        bS[4 * h + j] = dp4a_sub(o[j], __dp4a(e[j], 0x01010101u, bS[4 * h + j]));
-                        bQ[4 * h + j] = __dp4a(e[j], e[j], bQ[4 * h + j]) - __dp4a(o[j], o[j], 0u);
-                    }
+                for (int j = 0; j < 4; ++j) {
+                    bS[4 * h + j] = __dp4a(w[j], 0x01010101u, bS[4 * h + j]);
+                    bQ[4 * h + j] = __dp4a(w[j], w[j], bQ[4 * h + j]);
                 }
             }
-            {
-                uint32_t TS = 0, TQ = 0;
+        }
+        __syncwarp();  // every lane is done with slot cs
+        ps = cs;
+        if (++cs == NS) { cs = 0; cph ^= 1u; }
+    }
+    if (pr) bb_exchange(xbuf, warp, lane, bS, bQ);
+    if (tdbg && lane == 0) tdbg[3] = bb_gtimer();
+
+    // ---- row items
+    const int dr = d * r, dr1 = d * (r + 1);
+    const int64_t dpitch = (int64_t)d * p.bin_pitch;
+    uint8_t* orow = obase + (int64_t)ystart * p.bin_pitch;
+    const uint8_t* lcol = ring + 4 * BB_BPL * lane;  // this lane's 32 bytes of a staged row
+    int y = ystart;
+    for (int k = nwarm; k < n_items; ++k, y += d, orow += dpitch) {
+        if (k + NS - 1 < n_items) {
+            // item k+NS-1 is a plain row item here (never the warm-up-covered first row)
+            BB_PERTURB(pid, 4 * (k + NS - 1));
+            uint8_t* E = ring + ps * 3 * NC;
+            const int y2 = y + d * (NS - 1);
+            if (bb_elect()) {
+                if (rag) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&full[ps], 3 * NC);
+                stage_row(E, x8E, y2 + dr, &full[ps], pol_E);
+                stage_row(E + NC, x8E, y2 - dr1, &full[ps], pol_O);
+                stage_row(E + 2 * NC, x8F, y2, &full[ps], pol_F);
+            }
+        }
+        mbar_wait(&full[cs], cph);
+        BB_PERTURB(pid, 4 * k + 1);
+        if (rag) rag_patch(k, cs);
+        const int soff = cs * 3 * NC;
+        // ---- column side: block sums, exclusive block prefix -> even / odd planes
+        if (!(k == nwarm && d > 0)) {
+            const uint4* E = reinterpret_cast<const uint4*>(lcol + soff);
+            const uint4* O = reinterpret_cast<const uint4*>(lcol + soff + NC);
 #pragma unroll
-                for (int j = 0; j < BB_BPL; ++j) { TS += bS[j]; TQ += bQ[j]; }
-                uint32_t iS = TS, iQ = TQ;
+            for (int h = 0; h < BB_BPL / 4; ++h) {
+                const uint4 ev = E[h], ov = O[h];  // rows outside the image: zeros
+                const uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
+                const uint32_t o[4] = {ov.x, ov.y, ov.z, ov.w};
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
-                    const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
-                    if (lane >= off) { iS += vs; iQ += vq; }
-                }
-                BB_PERTURB(pid, 4 * k + 2);
-                // lane's exclusive prefix P[16 lane + j]: even j -> even plane, odd j -> odd plane
-                uint32_t vS = iS - TS, vQ = iQ - TQ;
-#pragma unroll
-                for (int h = 0; h < BB_BPL / 8; ++h) {
-                    uint32_t eS[4], oS[4], eQ[4], oQ[4];
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        eS[m] = vS; eQ[m] = vQ;
-                        vS += bS[8 * h + 2 * m]; vQ += bQ[8 * h + 2 * m];
-                        oS[m] = vS; oQ[m] = vQ;
-                        vS += bS[8 * h + 2 * m + 1]; vQ += bQ[8 * h + 2 * m + 1];
-                    }
-                    const int w = (BB_BPL / 2) * lane + 4 * h;
-                    *reinterpret_cast<uint4*>(PSe + w) = make_uint4(eS[0], eS[1], eS[2], eS[3]);
-                    *reinterpret_cast<uint4*>(PSe + PLW + w) = make_uint4(oS[0], oS[1], oS[2], oS[3]);
-                    *reinterpret_cast<uint4*>(PQe + w) = make_uint4(eQ[0], eQ[1], eQ[2], eQ[3]);
-                    *reinterpret_cast<uint4*>(PQe + PLW + w) = make_uint4(oQ[0], oQ[1], oQ[2], oQ[3]);
-                }
-                if (lane == 31) {  // P[NB]
-                    PSe[NB / 2] = iS;
-                    PQe[NB / 2] = iQ;
+                for (int j = 0; j < 4; ++j) {
+                    bS[4 * h + j] = dp4a_sub(o[j], __dp4a(e[j], 0x01010101u, bS[4 * h + j]));
+                    bQ[4 * h + j] = __dp4a(e[j], e[j], bQ[4 * h + j]) - __dp4a(o[j], o[j], 0u);
                 }
             }
-            __syncwarp();
-            BB_PERTURB(pid, 4 * k + 3);
-            // ---- output side: groups of 8 pixels
-            const uint8_t* F = stage + 2 * NC;
-            const int ny = min(y + r, p.H - 1) - max(y - r, 0) + 1;
-            const float rn = (ny == W) ? rnW : rcp_ftz((float)(ny * W));
-            const float rlo = rn * kUp, rhi = rn * kDn;
-            const uint32_t nU = (uint32_t)ny * nUc;
-            uint8_t* orow = obase + (int64_t)y * p.bin_pitch;
-            uint32_t um = 0;
-            // one interior group: bounds -> provisional bytes (stored) -> uncertain flag in um
-            auto group = [&](int i) {
+        }
+        {
+            uint32_t TS = 0, TQ = 0;
+#pragma unroll
+            for (int j = 0; j < BB_BPL; ++j) { TS += bS[j]; TQ += bQ[j]; }
+            uint32_t iS = TS, iQ = TQ;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
+                const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
+                if (lane >= off) { iS += vs; iQ += vq; }
+            }
+            BB_PERTURB(pid, 4 * k + 2);
+            // lane's exclusive prefix P[16 lane + j]: even j -> even plane, odd j -> odd plane
+            uint32_t vS = iS - TS, vQ = iQ - TQ;
+#pragma unroll
+            for (int h = 0; h < BB_BPL / 8; ++h) {
+                uint32_t eS[4], oS[4], eQ[4], oQ[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    eS[m] = vS; eQ[m] = vQ;
+                    vS += bS[8 * h + 2 * m]; vQ += bQ[8 * h + 2 * m];
+                    oS[m] = vS; oQ[m] = vQ;
+                    vS += bS[8 * h + 2 * m + 1]; vQ += bQ[8 * h + 2 * m + 1];
+                }
+                const int w = (BB_BPL / 2) * lane + 4 * h;
+                *reinterpret_cast<uint4*>(PSe + w) = make_uint4(eS[0], eS[1], eS[2], eS[3]);
+                *reinterpret_cast<uint4*>(PSe + PLW + w) = make_uint4(oS[0], oS[1], oS[2], oS[3]);
+                *reinterpret_cast<uint4*>(PQe + w) = make_uint4(eQ[0], eQ[1], eQ[2], eQ[3]);
+                *reinterpret_cast<uint4*>(PQe + PLW + w) = make_uint4(oQ[0], oQ[1], oQ[2], oQ[3]);
+            }
+            if (lane == 31) {  // P[NB]
+                PSe[NB / 2] = iS;
+                PQe[NB / 2] = iQ;
+            }
+        }
+        __syncwarp();
+        BB_PERTURB(pid, 4 * k + 3);
+        // ---- output side: groups of 8 pixels
+        const uint8_t* F = ring + soff + 2 * NC;
+        const int ny = min(y + r, p.H - 1) - max(y - r, 0) + 1;
+        const float rn = (ny == W) ? rnW : rcp_ftz((float)(ny * W));
+        const float rlo = rn * kUp, rhi = rn * kDn;
+        const uint32_t nU = (uint32_t)ny * nUc;
+        // one interior group, hot path only: group bounds -> provisional bytes (stored); a group
+        // with an open pixel is flagged in um1 and refined below (one out-of-line copy of the
+        // rare code keeps the unrolled hot path short: instruction-cache footprint)
+        uint32_t um = 0, um1 = 0;
+        auto group = [&](int i) {
+            const int g = lane + 32 * i;
+            const uint32_t sI = pSiH[32 * i] - pSiL[32 * i];
+            const uint32_t sU = pSuH[32 * i] - pSuL[32 * i];
+            const uint32_t qU = pSuH[2 * PLW + 32 * i] - pSuL[2 * PLW + 32 * i];
+            const float mlo = (float)sI * rhi;
+            const float mhi = (float)sU * rlo;
+            const uint32_t c = __float2uint_rz(mlo);
+            const uint32_t E = qU + c * (nU * c - 2u * sU);  // sum_{U'} (f - c)^2, exact
+            const float sd = sqrt_ftz((float)E * rlo);
+            const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sd, cK_up, a_up), tol), 4096.f);
+            const uint32_t H2 = bb_ceil2(thi);
+            const uint32_t L2 = bb_ceil2(__fmaf_rn(mlo, a_dn, -tol));
+            const uint2 fv = *reinterpret_cast<const uint2*>(F + 8 * g);
+            const uint32_t fA0 = prmt(fv.x, 0x80808080u, 0x4240), fB0 = prmt(fv.x, 0x80808080u, 0x4341);
+            const uint32_t fA1 = prmt(fv.y, 0x80808080u, 0x4240), fB1 = prmt(fv.y, 0x80808080u, 0x4341);
+            const uint32_t wA0 = fA0 - H2, wB0 = fB0 - H2, wA1 = fA1 - H2, wB1 = fB1 - H2;
+            const uint32_t o0 = prmt(wA0, wB0, 0xFBD9);  // bytes 0xFF where f >= ceil(t_hi)
+            const uint32_t o1 = prmt(wA1, wB1, 0xFBD9);
+            const uint32_t u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
+                                ((fB1 - L2) & ~wB1)) & 0x80008000u;
+            if (u) um1 |= 1u << i;
+            uint8_t* op = orow + X0 + 8 * g;
+            if (vec_ok) {  // provisional bytes (an open group is rewritten below)
+                __stcs(reinterpret_cast<uint2*>(op), make_uint2(o0, o1));
+            } else {
+                for (int j = 0; j < 8; ++j) op[j] = (uint8_t)((j < 4 ? o0 : o1) >> (8 * (j & 3)));
+            }
+        };
+#pragma unroll
+        for (int i = 0; i < BB_GPL; ++i)
+            if ((imask >> i) & 1u) group(i);
+        // open groups (~1e-4 of the C4 page's): a tighter lower bound from I'
+        // (n var(x) >= sum_I' (f - m_I')^2 = E_I - d^2/n_I), then per-pixel block bounds; what
+        // is still open goes to the exact path (um)
+        if (__builtin_expect(um1 != 0u, 0)) {
+#pragma unroll 1
+            for (uint32_t m1 = um1; m1; m1 &= m1 - 1) {
+                const int i = __ffs(m1) - 1;
                 const int g = lane + 32 * i;
                 const int x0 = X0 + 8 * g;
                 const uint32_t sI = pSiH[32 * i] - pSiL[32 * i];
                 const uint32_t sU = pSuH[32 * i] - pSuL[32 * i];
                 const uint32_t qU = pSuH[2 * PLW + 32 * i] - pSuL[2 * PLW + 32 * i];
+                const uint32_t qI = pSiH[2 * PLW + 32 * i] - pSiL[2 * PLW + 32 * i];
                 const float mlo = (float)sI * rhi;
                 const float mhi = (float)sU * rlo;
                 const uint32_t c = __float2uint_rz(mlo);
-                const uint32_t E = qU + c * (nU * c - 2u * sU);  // sum_{U'} (f - c)^2, exact
+                const uint32_t E = qU + c * (nU * c - 2u * sU);
                 const float sd = sqrt_ftz((float)E * rlo);
                 const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sd, cK_up, a_up), tol), 4096.f);
                 const uint32_t H2 = bb_ceil2(thi);
-                uint32_t L2 = bb_ceil2(__fmaf_rn(mlo, a_dn, -tol));
+                const uint32_t nI = (uint32_t)ny * nIc;
+                const uint32_t EI = qI + c * (nI * c - 2u * sI);
+                const float dd = (float)(int)(sI - nI * c);
+                const float v = __fmaf_rn(-(dd * dd) * kUp, rcp_ftz((float)nI) * kUp, (float)EI * kDn);
+                const float slo = sqrt_ftz(fmaxf(v, 0.f) * rhi) * kDn;
+                const uint32_t L2 = bb_ceil2(__fmaf_rn(mlo, __fmaf_rn(slo, cK_dn, a_dn), -tol));
                 const uint2 fv = *reinterpret_cast<const uint2*>(F + 8 * g);
                 const uint32_t fA0 = prmt(fv.x, 0x80808080u, 0x4240), fB0 = prmt(fv.x, 0x80808080u, 0x4341);
                 const uint32_t fA1 = prmt(fv.y, 0x80808080u, 0x4240), fB1 = prmt(fv.y, 0x80808080u, 0x4341);
                 const uint32_t wA0 = fA0 - H2, wB0 = fB0 - H2, wA1 = fA1 - H2, wB1 = fB1 - H2;
-                uint32_t o0 = prmt(wA0, wB0, 0xFBD9);  // bytes 0xFF where f >= ceil(t_hi)
-                uint32_t o1 = prmt(wA1, wB1, 0xFBD9);
-                uint32_t u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
-                              ((fB1 - L2) & ~wB1)) & 0x80008000u;
-                if (__builtin_expect(u != 0u, 0)) {
-                    // tighter lower bound: n var(x) >= sum_I' (f - m_I')^2 = E_I - d^2/n_I
-                    const uint32_t qI = pSiH[2 * PLW + 32 * i] - pSiL[2 * PLW + 32 * i];
-                    const uint32_t nI = (uint32_t)ny * nIc;
-                    const uint32_t EI = qI + c * (nI * c - 2u * sI);
-                    const float d = (float)(int)(sI - nI * c);
-                    const float v = __fmaf_rn(-(d * d) * kUp, rcp_ftz((float)nI) * kUp, (float)EI * kDn);
-                    const float slo = sqrt_ftz(fmaxf(v, 0.f) * rhi) * kDn;
-                    L2 = bb_ceil2(__fmaf_rn(mlo, __fmaf_rn(slo, cK_dn, a_dn), -tol));
-                    u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
-                         ((fB1 - L2) & ~wB1)) & 0x80008000u;
-                    if (u && !bb_pixel_refine(PSe, PQe, fv, alpha + 8 * g, x0, xc0, p.cols, r, ny, a_up, a_dn,
-                                              cK_up, cK_dn, tol, o0, o1))
-                        u = 0;
-                }
-                if (u) um |= 1u << i;
-                if (vec_ok) {  // provisional bytes (an uncertain group is rewritten below)
+                uint32_t o0 = prmt(wA0, wB0, 0xFBD9), o1 = prmt(wA1, wB1, 0xFBD9);
+                const uint32_t u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
+                                    ((fB1 - L2) & ~wB1)) & 0x80008000u;
+                if (!u) continue;  // every open pixel is below the tighter ceil(t_lo): black, as stored
+                if (bb_pixel_refine(PSe, PQe, fv, alpha + 8 * g, x0, xc0, p.cols, r, ny, a_up, a_dn, cK_up,
+                                    cK_dn, tol, o0, o1))
+                    um |= 1u << i;
+                if (vec_ok) {
                     __stcs(reinterpret_cast<uint2*>(orow + x0), make_uint2(o0, o1));
                 } else {
                     for (int j = 0; j < 8; ++j) orow[x0 + j] = (uint8_t)((j < 4 ? o0 : o1) >> (8 * (j & 3)));
                 }
-            };
+            }
+        }
+        if (edge_strip) {
+            // groups whose windows the image's left / right edge clips: per-pixel bounds, the
+            // warp's lanes over their pixels (left groups [0, gl), right groups [gr, ngv))
+            const int nbp = 8 * (gl + ngv - gr);
+            for (int q0 = 0; q0 < nbp; q0 += 64) {  // two pixels per lane per pass (ILP)
+                int v[2];
 #pragma unroll
-            for (int i = 0; i < BB_GPL; ++i)
-                if ((imask >> i) & 1u) group(i);
-            if (edge_strip) {
-                // groups whose windows the image's left / right edge clips: per-pixel bounds, the
-                // warp's lanes over their pixels (left groups [0, gl), right groups [gr, ngv))
-                const int nbp = 8 * (gl + ngv - gr);
-                for (int q0 = 0; q0 < nbp; q0 += 64) {  // two pixels per lane per pass (ILP)
-                    int v[2];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int q = q0 + 32 * h + lane;
-                        v[h] = 0x100;  // no pixel
-                        if (q < nbp) {
-                            const int gq = (q >> 3) < gl ? (q >> 3) : gr + (q >> 3) - gl, j = q & 7;
-                            const int x = X0 + 8 * gq + j;
-                            if (x < p.cols)
-                                v[h] = bb_pixel_decide(PSe, PQe, F[8 * gq + j], alpha + 8 * gq + j, x, xc0,
-                                                       p.cols, r, ny, a_up, a_dn, cK_up, cK_dn, tol);
-                        }
-                    }
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int q = q0 + 32 * h + lane;
+                for (int h = 0; h < 2; ++h) {
+                    const int q = q0 + 32 * h + lane;
+                    v[h] = 0x100;  // no pixel
+                    if (q < nbp) {
                         const int gq = (q >> 3) < gl ? (q >> 3) : gr + (q >> 3) - gl, j = q & 7;
-                        if (v[h] != 0x100) orow[X0 + 8 * gq + j] = (uint8_t)(v[h] & 0xFF);
-                        unsigned ob = __ballot_sync(0xffffffffu, v[h] < 0);
-                        while (ob) {  // owners of groups with an open pixel
-                            const int qb = q0 + 32 * h + __ffs(ob) - 1;
-                            ob &= ob - 1;
-                            const int gb = (qb >> 3) < gl ? (qb >> 3) : gr + (qb >> 3) - gl;
-                            if ((gb & 31) == lane) um |= 1u << (gb >> 5);
-                        }
+                        const int x = X0 + 8 * gq + j;
+                        if (x < p.cols)
+                            v[h] = bb_pixel_decide(PSe, PQe, F[8 * gq + j], alpha + 8 * gq + j, x, xc0,
+                                                   p.cols, r, ny, a_up, a_dn, cK_up, cK_dn, tol);
                     }
                 }
-                __syncwarp();  // the byte stores above precede an owner's exact rewrite below
-            }
-            // uncertain groups: exact per-pixel re-decision, one group at a time by the warp
-            while (__any_sync(0xffffffffu, um != 0u)) {
-                const unsigned bal = __ballot_sync(0xffffffffu, um != 0u);
-                const int src = __ffs(bal) - 1;
-                const int slot = __shfl_sync(0xffffffffu, um ? __ffs(um) - 1 : 0, src);
-                const int g = src + 32 * slot;
-                const uint2 wv = bb_exact_group<SEG>(&p, in0, PSe, PQe, F, g, y, X0, xc0, alpha, ny);
-                if (tdbg && lane == 0) tdbg[2] += 1;
-                if (lane == src) {
-                    um &= ~(1u << slot);
-                    const int x0 = X0 + 8 * g;
-                    if (vec_ok && x0 + 8 <= p.cols) {
-                        __stcs(reinterpret_cast<uint2*>(orow + x0), wv);
-                    } else {
-                        for (int j = 0; j < 8 && x0 + j < p.cols; ++j)
-                            orow[x0 + j] = (uint8_t)((j < 4 ? wv.x : wv.y) >> (8 * (j & 3)));
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int q = q0 + 32 * h + lane;
+                    const int gq = (q >> 3) < gl ? (q >> 3) : gr + (q >> 3) - gl, j = q & 7;
+                    if (v[h] != 0x100) orow[X0 + 8 * gq + j] = (uint8_t)(v[h] & 0xFF);
+                    unsigned ob = __ballot_sync(0xffffffffu, v[h] < 0);
+                    while (ob) {  // owners of groups with an open pixel
+                        const int qb = q0 + 32 * h + __ffs(ob) - 1;
+                        ob &= ob - 1;
+                        const int gb = (qb >> 3) < gl ? (qb >> 3) : gr + (qb >> 3) - gl;
+                        if ((gb & 31) == lane) um |= 1u << (gb >> 5);
                     }
+                }
+            }
+            __syncwarp();  // the byte stores above precede an owner's exact rewrite below
+        }
+        // uncertain groups: exact per-pixel re-decision, one group at a time by the warp
+        while (__any_sync(0xffffffffu, um != 0u)) {
+            const unsigned bal = __ballot_sync(0xffffffffu, um != 0u);
+            const int src = __ffs(bal) - 1;
+            const int slot = __shfl_sync(0xffffffffu, um ? __ffs(um) - 1 : 0, src);
+            const int g = src + 32 * slot;
+            const uint2 wv = bb_exact_group<SEG>(&p, in0, PSe, PQe, F, g, y, X0, xc0, alpha, ny);
+            if (tdbg && lane == 0) tdbg[2] += 1;
+            if (lane == src) {
+                um &= ~(1u << slot);
+                const int x0 = X0 + 8 * g;
+                if (vec_ok && x0 + 8 <= p.cols) {
+                    __stcs(reinterpret_cast<uint2*>(orow + x0), wv);
+                } else {
+                    for (int j = 0; j < 8 && x0 + j < p.cols; ++j)
+                        orow[x0 + j] = (uint8_t)((j < 4 ? wv.x : wv.y) >> (8 * (j & 3)));
                 }
             }
         }
-        __syncwarp();  // every lane is done with slot s (and, for a row, with the prefix)
+        __syncwarp();  // every lane is done with slot cs and with the prefix planes
+        ps = cs;
+        if (++cs == NS) { cs = 0; cph ^= 1u; }
     }
-    if (pr && nmain == 0) bb_exchange(xbuf, warp, lane, bS, bQ);  // the partner still needs our half
     if (tdbg && lane == 0) tdbg[1] = bb_gtimer();
 }
 

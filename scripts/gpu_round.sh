@@ -15,3 +15,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --c
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_ncu_launch.log 2>&1; echo launches=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"bb_kernel" -s 2 -c 1 -o $O/${TAG}_prof_bb \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_ncu.log 2>&1; echo ncu=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"bb_kernel" -s 6 -c 1 -o $O/${TAG}_prof_band \
+  python bench.py --emulate-bands 8 --steps 3 --warmup 3 > $O/${TAG}_ncu_band.log 2>&1; echo ncu_band=$?
