@@ -146,17 +146,16 @@ __device__ __forceinline__ uint32_t bb_sel3(const uint32_t (&w)[3], int i) {
     return i == 0 ? w[0] : (i == 1 ? w[1] : w[2]);
 }
 
-// Exact re-decision of group g (8 pixels) of output row y by the whole warp.  A pixel's window
-// [a, a+2r] (strip columns, a = alpha+8g+j) is its block part [4 blo, 4 bhi) from the prefix plus
-// a partial word on each side: bytes (a&3).. of the word holding a, and bytes ..(a+2r)&3 of the
-// word at 4 bhi.  Lanes take the window rows 32 apart and accumulate those partial words with
-// dp4a; a butterfly sums them; lane j finishes pixel j (certified fp32 decision, fp64 replay
-// within tol).  Returns the group's two output words (every lane).
+// Exact re-decision of the pixels `pmask` of group g (8 pixels) of output row y by the whole
+// warp.  A pixel's window [a, a+2r] (strip columns, a = alpha+8g+j) is its block part
+// [4 blo, 4 bhi) from the prefix plus a partial word on each side: bytes (a&3).. of the word
+// holding a, and bytes ..(a+2r)&3 of the word at 4 bhi.  Lanes take the window rows 32 apart (all
+// loads in flight together) and accumulate those partial words with dp4a; a butterfly sums them;
+// lane 0 finishes the pixel (certified fp32 decision, fp64 replay within tol) and stores its byte.
 template <bool SEG>
-__device__ __forceinline__ uint2 bb_exact_group(const SlideParams* pp, const uint8_t* in0,
-                                             const uint32_t* PS, const uint32_t* PQ,
-                                             const uint8_t* F, int g, int y, int X0, int xc0,
-                                             int alpha, int ny) {
+__device__ __forceinline__ void bb_exact_pixels(const SlideParams* pp, const uint8_t* in0, const uint32_t* PS,
+                                                const uint32_t* PQ, const uint8_t* F, int g, int y, int X0,
+                                                int xc0, int alpha, int ny, uint32_t pmask, uint8_t* orow) {
     const SlideParams& p = *pp;
     const int lane = threadIdx.x & 31;
     const int r = p.r;
@@ -164,63 +163,50 @@ __device__ __forceinline__ uint2 bb_exact_group(const SlideParams* pp, const uin
     const int a0 = alpha + 8 * g;
     const int baseL = a0 & ~3;
     const int baseR = (a0 + 2 * r + 1) & ~3;
-    uint32_t S[8], Q[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) { S[j] = 0; Q[j] = 0; }
     const int r0 = max(y - r, 0), r1 = min(y + r, p.H - 1);
-    // rows r0 + lane + 32 m: all loads of a 4-row batch are in flight together
-    for (int rb = r0 + lane; rb - lane <= r1; rb += 128) {
-        uint32_t wl[4][3], wr[4][3];
+    uint32_t wl[8][3], wr[8][3];  // rows r0 + lane + 32 m (W <= 255: at most 8 per lane)
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const int row = rb + 32 * m;
-            if (row <= r1) {
-                const uint8_t* rp = row_at<SEG>(p, in0, row);
-                bb_words3(rp, xc0 + baseL, p.cols, wl[m]);
-                bb_words3(rp, xc0 + baseR, p.cols, wr[m]);
-            } else {
-                wl[m][0] = wl[m][1] = wl[m][2] = wr[m][0] = wr[m][1] = wr[m][2] = 0;
-            }
-        }
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int a = a0 + j, b = a + 2 * r + 1;  // window [a, b)
-                const int lo = a & 3, hi = b & 3;
-                const uint32_t ml = lo ? (0xFFFFFFFFu << (8 * lo)) : 0u;
-                const uint32_t mr = hi ? (0xFFFFFFFFu >> (32 - 8 * hi)) : 0u;
-                const uint32_t xl = bb_sel3(wl[m], (a - baseL) >> 2) & ml;
-                const uint32_t xr = bb_sel3(wr[m], ((b & ~3) - baseR) >> 2) & mr;
-                S[j] = __dp4a(xl, 0x01010101u, __dp4a(xr, 0x01010101u, S[j]));
-                Q[j] = __dp4a(xl, xl, __dp4a(xr, xr, Q[j]));
-            }
+    for (int m = 0; m < 8; ++m) {
+        const int row = r0 + lane + 32 * m;
+        if (row <= r1) {
+            const uint8_t* rp = row_at<SEG>(p, in0, row);
+            bb_words3(rp, xc0 + baseL, p.cols, wl[m]);
+            bb_words3(rp, xc0 + baseR, p.cols, wr[m]);
+        } else {
+            wl[m][0] = wl[m][1] = wl[m][2] = wr[m][0] = wr[m][1] = wr[m][2] = 0;
         }
     }
+#pragma unroll 1
+    for (uint32_t pmm = pmask; pmm; pmm &= pmm - 1) {
+        const int j = __ffs(pmm) - 1;
+        const int a = a0 + j, b = a + 2 * r + 1;  // window [a, b)
+        const int lo = a & 3, hi = b & 3;
+        const uint32_t ml = lo ? (0xFFFFFFFFu << (8 * lo)) : 0u;
+        const uint32_t mr = hi ? (0xFFFFFFFFu >> (32 - 8 * hi)) : 0u;
+        const int il = (a - baseL) >> 2, ir = ((b & ~3) - baseR) >> 2;
+        uint32_t Sx = 0, Qx = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+        for (int m = 0; m < 8; ++m) {
+            const uint32_t xl = bb_sel3(wl[m], il) & ml;
+            const uint32_t xr = bb_sel3(wr[m], ir) & mr;
+            Sx = __dp4a(xl, 0x01010101u, __dp4a(xr, 0x01010101u, Sx));
+            Qx = __dp4a(xl, xl, __dp4a(xr, xr, Qx));
+        }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            S[j] += __shfl_xor_sync(0xffffffffu, S[j], off);
-            Q[j] += __shfl_xor_sync(0xffffffffu, Q[j], off);
+            Sx += __shfl_xor_sync(0xffffffffu, Sx, off);
+            Qx += __shfl_xor_sync(0xffffffffu, Qx, off);
         }
-    }
-    uint32_t Sx = 0, Qx = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (lane == j) { Sx = S[j]; Qx = Q[j]; }
-    uint32_t white = 0;
-    if (lane < 8) {
-        const int a = a0 + lane;
-        const int blo = (a + 3) >> 2, bhi = (a + 2 * r + 1) >> 2;
-        Sx += bb_pre(PS, bhi) - bb_pre(PS, blo);
-        Qx += bb_pre(PQ, bhi) - bb_pre(PQ, blo);
-        const int x = X0 + 8 * g + lane;
-        if (x < p.cols) {
-            const uint32_t f = F[8 * g + lane];
+        const int x = X0 + 8 * g + j;
+        if (lane == 0 && x < p.cols) {
+            const int blo = (a + 3) >> 2, bhi = b >> 2;
+            Sx += bb_pre(PS, bhi) - bb_pre(PS, blo);
+            Qx += bb_pre(PQ, bhi) - bb_pre(PQ, blo);
+            const uint32_t f = F[8 * g + j];
             const int nx = min(x + r, p.cols - 1) - max(x - r, 0) + 1;
             const uint32_t n = (uint32_t)(ny * nx);
             const float d = fast_diff<DTB_METHOD_SAUVOLA, true>(Sx, Qx, f, n, p.cA, p.cC, p.a, p.c);
+            uint32_t white;
             if (fabsf(d) >= p.tol) {
                 white = d < 0.f ? 0u : 0xFFu;
             } else {
@@ -236,12 +222,9 @@ __device__ __forceinline__ uint2 bb_exact_group(const SlideParams* pp, const uin
                     }
                 }
             }
+            orow[x] = (uint8_t)white;
         }
     }
-    uint32_t v = white << (8 * (lane & 3));
-    v |= __shfl_xor_sync(0xffffffffu, v, 1);
-    v |= __shfl_xor_sync(0xffffffffu, v, 2);
-    return make_uint2(__shfl_sync(0xffffffffu, v, 0), __shfl_sync(0xffffffffu, v, 4));
 }
 
 // Per-pixel bounds for the pixel at image column x (strip column a = start of its window):
@@ -277,24 +260,18 @@ __device__ __forceinline__ int bb_pixel_decide(const uint32_t* PS, const uint32_
     return ff < tlo ? 0 : (ff >= thi ? 0xFF : -1);
 }
 
-// An interior group the group bounds left open: per-pixel bounds for its 8 pixels.  Rewrites
-// the decided bytes of (o0, o1); returns whether some pixel is still open.
-__device__ __forceinline__ bool bb_pixel_refine(const uint32_t* PS, const uint32_t* PQ, uint2 fv, int a0, int x0,
-                                                int xc0, int cols, int r, int ny, float a_up, float a_dn,
-                                                float cK_up, float cK_dn, float tol, uint32_t& o0, uint32_t& o1) {
-    bool open = false;
-    uint32_t ob[2] = {o0, o1};
-#pragma unroll 1
-    for (int j = 0; j < 8; ++j) {
-        const uint32_t sh = 8 * (j & 3);
-        const int v = bb_pixel_decide(PS, PQ, ((j < 4 ? fv.x : fv.y) >> sh) & 0xFFu, a0 + j, x0 + j, xc0, cols,
-                                      r, ny, a_up, a_dn, cK_up, cK_dn, tol);
-        if (v < 0) open = true;
-        else ob[j >> 2] = (ob[j >> 2] & ~(0xFFu << sh)) | ((uint32_t)v << sh);
+// Count bounds of the edge group g (pixels x0..x0+7 inside the page): the smallest and largest
+// clipped window width over its pixels and the in-image columns of U', packed 10 + 10 + 12 bits.
+__device__ __forceinline__ uint32_t bb_edge_consts(int x0, int g, int xc0, int uL, int uH, int r, int cols) {
+    const int xl = min(x0 + 7, cols - 1);
+    int nxmin = 0x3FF, nxmax = 0;
+    for (int x = x0; x <= xl; ++x) {
+        const int nx = min(x + r, cols - 1) - max(x - r, 0) + 1;
+        nxmin = min(nxmin, nx);
+        nxmax = max(nxmax, nx);
     }
-    o0 = ob[0];
-    o1 = ob[1];
-    return open;
+    const int cu = min(xc0 + 4 * (2 * g + uH), cols) - max(xc0 + 4 * (2 * g + uL), 0);
+    return (uint32_t)nxmin | ((uint32_t)nxmax << 10) | ((uint32_t)cu << 20);
 }
 
 // Opaque copies: the value must live in a register from here on (ptxas cannot re-derive it).
@@ -309,6 +286,18 @@ __device__ __forceinline__ uint32_t bb_pin(uint32_t v) {
 __device__ __forceinline__ float bb_pinf(float v) {
     asm volatile("" : "+f"(v));
     return v;
+}
+
+// One step of the inclusive warp scan of (s, q): shfl.up's own predicate (lane >= off) guards
+// the adds, one instruction each.
+__device__ __forceinline__ void bb_scan_step(uint32_t& s, uint32_t& q, int off) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t.reg .b32 T;\n\t"
+        "shfl.sync.up.b32 T|P, %0, %2, 0, 0xffffffff;\n\t"
+        "@P add.u32 %0, %0, T;\n\t"
+        "shfl.sync.up.b32 T|P, %1, %2, 0, 0xffffffff;\n\t"
+        "@P add.u32 %1, %1, T;\n\t}"
+        : "+r"(s), "+r"(q) : "r"(off));
 }
 
 __device__ __forceinline__ bool bb_elect() {
@@ -355,7 +344,8 @@ struct BBMaps {
 template <bool SEG, int MINB>
 __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ SlideParams p,
                                                       const __grid_constant__ BBMaps mp,
-                                                      int nstrips, int npairs, int tw0, int paired) {
+                                                      int nstrips, int npairs, int tw0, int paired,
+                                                      int npairs_e, int th_e, int skew) {
     constexpr int NS = BB_STAGES, NC = BB_NC, NB = BB_NB, PLW = BB_PLW;
     extern __shared__ __align__(128) uint8_t smb[];
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform for the compiler
@@ -369,8 +359,29 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
     unsigned long long* const tdbg = (g_bb_times && pid < g_bb_times_cap) ? g_bb_times + 4 * pid : nullptr;
     if (tdbg && lane == 0) { tdbg[2] = 0; tdbg[3] = 0; }
     if (tdbg && lane == 0) tdbg[0] = bb_gtimer();
-    const int strip = (int)blockIdx.x % nstrips, rest = (int)blockIdx.x / nstrips;
-    const int pair = rest % npairs, img = rest / npairs;
+    // blockIdx.x -> (strip, band pair, image).  npairs_e > 0: the two edge strips (costlier rows)
+    // have their own, shorter bands -- th_e rows, npairs_e pairs -- after the interior strips' CTAs
+    int strip, pair, img, TH = p.TH;
+    if (npairs_e == 0) {
+        strip = (int)blockIdx.x % nstrips;
+        const int rest = (int)blockIdx.x / nstrips;
+        pair = rest % npairs;
+        img = rest / npairs;
+    } else {
+        // (the edge CTAs come first: the SM's warp schedulers favour older warps, and the edge
+        // pipelines are the ones that set the kernel time)
+        const int n_edge = 2 * npairs_e, cpi = (nstrips - 2) * npairs + n_edge;
+        const int idx = (int)blockIdx.x % cpi;
+        img = (int)blockIdx.x / cpi;
+        if (idx < n_edge) {
+            strip = (idx & 1) ? nstrips - 1 : 0;
+            pair = idx >> 1;
+            TH = th_e;
+        } else {
+            strip = 1 + (idx - n_edge) % (nstrips - 2);
+            pair = (idx - n_edge) / (nstrips - 2);
+        }
+    }
     const int r = p.r;
     const int alpha = (16 - (r & 15)) & 15;
     // strip widths: the first strip tw0 (narrower: its edge groups cost per-pixel bounds), the
@@ -380,14 +391,26 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
     const int xc0 = X0 - r - alpha;
     // B = first row of band 2j+1 (or the end of the output rows); warp 0 outputs [B, yb) going
     // down, warp 1 outputs [ya, B) going up
-    const int ya_up = p.out_begin + 2 * pair * p.TH;
-    const int B = min(ya_up + p.TH, p.out_end);
+    // band b of nbc starts at row S(b).  skew == 0: S(b) = b TH.  Otherwise the bands shrink
+    // linearly with the CTA index, from (1 + skew/256) to (1 - skew/256) of the mean height: the
+    // SM's warp schedulers favour older warps, so later CTAs run measurably slower
+    // (C4 timeline: 188 -> 225 us from the first to the last octile of CTAs at equal heights).
+    const int rows_out = p.out_end - p.out_begin;
+    const int nbc = (strip == 0 || strip == nstrips - 1) && npairs_e ? 2 * npairs_e : 2 * npairs;
+    auto S = [&](int b) {
+        if (!skew) return min(p.out_begin + b * TH, p.out_end);
+        if (b >= nbc) return p.out_end;
+        const long long num = (long long)b * (256 + skew) * nbc - (long long)skew * b * b;
+        return p.out_begin + (int)((long long)rows_out * num / (256ll * nbc * nbc));
+    };
+    const int ya_up = S(2 * pair);
+    const int B = S(2 * pair + 1);
     // paired == 0 (tall bands, where the warm-up is a small share): both warps run downward
     // bands with their own warm-ups (band 2j from ya_up, band 2j+1 from B)
     const bool pr = paired != 0;
     const int d = (warp == 0 || !pr) ? 1 : -1;
     const int ystart = warp == 0 ? B : (pr ? B - 1 : ya_up);
-    const int nmain = warp == 0 ? max(min(B + p.TH, p.out_end) - B, 0) : B - ya_up;
+    const int nmain = warp == 0 ? S(2 * pair + 2) - B : B - ya_up;
     const uint8_t* in0 = p.in + (int64_t)img * p.img_stride - (int64_t)p.row0 * p.pitch;
     // warm-up window [Bw - r, Bw + r] (clipped), items of 3 rows; paired: the shared window at B,
     // warp 0 takes the first half of the items, warp 1 the rest
@@ -450,22 +473,28 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
         bb_pin((int)((((uintptr_t)p.bin | (uintptr_t)p.bin_pitch | (uintptr_t)p.out_stride) & 7) == 0)) != 0;
     // group slots of this lane: imask = interior groups (all 8 windows inside the image in x)
     uint32_t imask = 0;
-    // (uniform) valid groups ngv; left-edge groups [0, gl), right-edge groups [gr, ngv)
-    const int ngv = min(TWs / 8, (p.cols - X0 + 7) / 8);
-    const int gl = min(ngv, max(0, (r - X0 + 7) / 8));
-    const int vr = p.cols - 7 - r - X0;  // right-edge groups: X0 + 8g >= vr
-    const int gr = max(gl, min(ngv, vr > 0 ? (vr + 7) / 8 : -((-vr) / 8)));
-    const bool edge_strip = gl > 0 || gr < ngv;
+    // emask = the lane's other valid groups: some window clipped by the image's left / right edge,
+    // or the ragged last group of the page (pixels past the last column)
+    uint32_t emask = 0;
 #pragma unroll
     for (int i = 0; i < BB_GPL; ++i) {
         const int g = lane + 32 * i, x0 = X0 + 8 * g;
         if (g < TWs / 8 && x0 < p.cols) {
             if (x0 - r >= 0 && x0 + 7 + r <= p.cols - 1) imask |= 1u << i;
+            else emask |= 1u << i;
         }
     }
     imask = bb_pin(imask);
+    emask = bb_pin(emask);
+    const int ei0 = emask ? __ffs(emask) - 1 : -1;
+    const uint32_t ecst =
+        bb_pin(ei0 >= 0 ? bb_edge_consts(X0 + 8 * (lane + 32 * ei0), lane + 32 * ei0, xc0, uL, uH, r, p.cols) : 0u);
+    // (uniform) slots holding some lane's interior group
+    const int nslots = 32 - __clz(__reduce_or_sync(0xffffffffu, imask));
     uint8_t* obase = p.bin + (int64_t)img * p.out_stride - (int64_t)p.out_begin * p.bin_pitch;
     const float rnW = 1.0f / (float)(W * W);  // interior rows: n = W^2
+    const float rloW = bb_pinf(rnW * kUp), rhiW = bb_pinf(rnW * kDn);
+    const uint32_t nUW = bb_pin((uint32_t)W * nUc);
 
     uint32_t bS[BB_BPL], bQ[BB_BPL];
 #pragma unroll
@@ -606,11 +635,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             for (int j = 0; j < BB_BPL; ++j) { TS += bS[j]; TQ += bQ[j]; }
             uint32_t iS = TS, iQ = TQ;
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t vs = __shfl_up_sync(0xffffffffu, iS, off);
-                const uint32_t vq = __shfl_up_sync(0xffffffffu, iQ, off);
-                if (lane >= off) { iS += vs; iQ += vq; }
-            }
+            for (int off = 1; off < 32; off <<= 1) bb_scan_step(iS, iQ, off);
             BB_PERTURB(pid, 4 * k + 2);
             // lane's exclusive prefix P[16 lane + j]: even j -> even plane, odd j -> odd plane
             uint32_t vS = iS - TS, vQ = iQ - TQ;
@@ -640,15 +665,23 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
         // ---- output side: groups of 8 pixels
         const uint8_t* F = ring + soff + 2 * NC;
         const int ny = min(y + r, p.H - 1) - max(y - r, 0) + 1;
-        const float rn = (ny == W) ? rnW : rcp_ftz((float)(ny * W));
-        const float rlo = rn * kUp, rhi = rn * kDn;
-        const uint32_t nU = (uint32_t)ny * nUc;
+        float rlo = rloW, rhi = rhiW;  // interior rows: n = W^2
+        uint32_t nU = nUW;
+        if (ny != W) {
+            const float rn = rcp_ftz((float)(ny * W));
+            rlo = rn * kUp;
+            rhi = rn * kDn;
+            nU = (uint32_t)ny * nUc;
+        }
         // one interior group, hot path only: group bounds -> provisional bytes (stored); a group
         // with an open pixel is flagged in um1 and refined below (one out-of-line copy of the
-        // rare code keeps the unrolled hot path short: instruction-cache footprint)
-        uint32_t um = 0, um1 = 0;
-        auto group = [&](int i) {
+        // rare code keeps the unrolled hot path short: instruction-cache footprint).  Every lane
+        // computes every slot (slots without an interior group read stale words of the planes and
+        // drop the result): no branches, so the slots interleave.
+        uint32_t um1 = 0;
+        auto group = [&](int i, bool vec) {
             const int g = lane + 32 * i;
+            const bool on = (imask >> i) & 1u;
             const uint32_t sI = pSiH[32 * i] - pSiL[32 * i];
             const uint32_t sU = pSuH[32 * i] - pSuL[32 * i];
             const uint32_t qU = pSuH[2 * PLW + 32 * i] - pSuL[2 * PLW + 32 * i];
@@ -668,26 +701,75 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             const uint32_t o1 = prmt(wA1, wB1, 0xFBD9);
             const uint32_t u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
                                 ((fB1 - L2) & ~wB1)) & 0x80008000u;
-            if (u) um1 |= 1u << i;
+            if (u && on) um1 |= 1u << i;
             uint8_t* op = orow + X0 + 8 * g;
-            if (vec_ok) {  // provisional bytes (an open group is rewritten below)
-                __stcs(reinterpret_cast<uint2*>(op), make_uint2(o0, o1));
-            } else {
+            if (vec) {  // provisional bytes (an open group is rewritten below)
+                if (on) __stcs(reinterpret_cast<uint2*>(op), make_uint2(o0, o1));
+            } else if (on) {
                 for (int j = 0; j < 8; ++j) op[j] = (uint8_t)((j < 4 ? o0 : o1) >> (8 * (j & 3)));
             }
         };
+        if (vec_ok && nslots == BB_GPL) {
 #pragma unroll
-        for (int i = 0; i < BB_GPL; ++i)
-            if ((imask >> i) & 1u) group(i);
-        // open groups (~1e-4 of the C4 page's): a tighter lower bound from I'
-        // (n var(x) >= sum_I' (f - m_I')^2 = E_I - d^2/n_I), then per-pixel block bounds; what
-        // is still open goes to the exact path (um)
-        if (__builtin_expect(um1 != 0u, 0)) {
+            for (int i = 0; i < BB_GPL; ++i) group(i, true);
+        } else if (vec_ok) {
+#pragma unroll
+            for (int i = 0; i < BB_GPL - 1; ++i) group(i, true);
+        } else {
 #pragma unroll 1
-            for (uint32_t m1 = um1; m1; m1 &= m1 - 1) {
+            for (int i = 0; i < BB_GPL; ++i) group(i, false);
+        }
+        // edge groups (windows clipped in x, or the ragged last group): the same block bounds --
+        // columns outside the image are staged as zeros, so S_I', S_U', Q_U' need no clipping --
+        // with the group's own count bounds: n_min <= n(x) <= n_max over its pixels, and the
+        // in-image pixel count of U' in E
+        if (emask) {
+#pragma unroll 1
+            for (uint32_t m1 = emask; m1; m1 &= m1 - 1) {
                 const int i = __ffs(m1) - 1;
                 const int g = lane + 32 * i;
-                const int x0 = X0 + 8 * g;
+                const int x0 = X0 + 8 * g, xl = min(x0 + 7, p.cols - 1);
+                // the lane's first edge group: constants packed in the prologue; further ones
+                // (pages narrower than two strips) are derived here
+                const uint32_t ec = i == ei0 ? ecst : bb_edge_consts(x0, g, X0 - r - alpha, uL, uH, r, p.cols);
+                const int nxmin = ec & 0x3FF, nxmax = (ec >> 10) & 0x3FF, cu = ec >> 20;
+                const float rhiG = rcp_ftz((float)(ny * nxmax)) * kDn, rloG = rcp_ftz((float)(ny * nxmin)) * kUp;
+                const uint32_t nUG = (uint32_t)(ny * cu);
+                const uint32_t sI = pSiH[32 * i] - pSiL[32 * i];
+                const uint32_t sU = pSuH[32 * i] - pSuL[32 * i];
+                const uint32_t qU = pSuH[2 * PLW + 32 * i] - pSuL[2 * PLW + 32 * i];
+                const float mlo = (float)sI * rhiG;
+                const float mhi = (float)sU * rloG;
+                const uint32_t c = __float2uint_rz(mlo);
+                const uint32_t E = qU + c * (nUG * c - 2u * sU);
+                const float sd = sqrt_ftz((float)E * rloG);
+                const float thi = fminf(__fmaf_rn(mhi, __fmaf_rn(sd, cK_up, a_up), tol), 4096.f);
+                const uint32_t H2 = bb_ceil2(thi);
+                const uint32_t L2 = bb_ceil2(__fmaf_rn(mlo, a_dn, -tol));
+                const uint2 fv = *reinterpret_cast<const uint2*>(F + 8 * g);
+                const uint32_t fA0 = prmt(fv.x, 0x80808080u, 0x4240), fB0 = prmt(fv.x, 0x80808080u, 0x4341);
+                const uint32_t fA1 = prmt(fv.y, 0x80808080u, 0x4240), fB1 = prmt(fv.y, 0x80808080u, 0x4341);
+                const uint32_t wA0 = fA0 - H2, wB0 = fB0 - H2, wA1 = fA1 - H2, wB1 = fB1 - H2;
+                const uint32_t o0 = prmt(wA0, wB0, 0xFBD9), o1 = prmt(wA1, wB1, 0xFBD9);
+                const uint32_t u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
+                                    ((fB1 - L2) & ~wB1)) & 0x80008000u;
+                if (u) um1 |= 1u << i;  // (an open lane past the last column only costs a refinement)
+                if (vec_ok && x0 + 8 <= p.cols) {
+                    __stcs(reinterpret_cast<uint2*>(orow + x0), make_uint2(o0, o1));
+                } else {
+                    for (int j = 0; x0 + j <= xl; ++j) orow[x0 + j] = (uint8_t)((j < 4 ? o0 : o1) >> (8 * (j & 3)));
+                }
+            }
+        }
+        // open groups (~1e-4 of the C4 page's, but clustered: dark regions).  Interior groups first
+        // try a tighter lower bound from I' (n var(x) >= sum_I' (f - m_I')^2 = E_I - d^2/n_I), each
+        // lane on its own groups.
+        if (__builtin_expect(um1 != 0u, 0)) {
+#pragma unroll 1
+            for (uint32_t m1 = um1 & imask; m1; m1 &= m1 - 1) {
+                const int i = __ffs(m1) - 1;
+                const int g = lane + 32 * i;
+                const uint2 fv = *reinterpret_cast<const uint2*>(F + 8 * g);
                 const uint32_t sI = pSiH[32 * i] - pSiL[32 * i];
                 const uint32_t sU = pSuH[32 * i] - pSuL[32 * i];
                 const uint32_t qU = pSuH[2 * PLW + 32 * i] - pSuL[2 * PLW + 32 * i];
@@ -705,76 +787,57 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
                 const float v = __fmaf_rn(-(dd * dd) * kUp, rcp_ftz((float)nI) * kUp, (float)EI * kDn);
                 const float slo = sqrt_ftz(fmaxf(v, 0.f) * rhi) * kDn;
                 const uint32_t L2 = bb_ceil2(__fmaf_rn(mlo, __fmaf_rn(slo, cK_dn, a_dn), -tol));
-                const uint2 fv = *reinterpret_cast<const uint2*>(F + 8 * g);
                 const uint32_t fA0 = prmt(fv.x, 0x80808080u, 0x4240), fB0 = prmt(fv.x, 0x80808080u, 0x4341);
                 const uint32_t fA1 = prmt(fv.y, 0x80808080u, 0x4240), fB1 = prmt(fv.y, 0x80808080u, 0x4341);
                 const uint32_t wA0 = fA0 - H2, wB0 = fB0 - H2, wA1 = fA1 - H2, wB1 = fB1 - H2;
-                uint32_t o0 = prmt(wA0, wB0, 0xFBD9), o1 = prmt(wA1, wB1, 0xFBD9);
                 const uint32_t u = (((fA0 - L2) & ~wA0) | ((fB0 - L2) & ~wB0) | ((fA1 - L2) & ~wA1) |
                                     ((fB1 - L2) & ~wB1)) & 0x80008000u;
-                if (!u) continue;  // every open pixel is below the tighter ceil(t_lo): black, as stored
-                if (bb_pixel_refine(PSe, PQe, fv, alpha + 8 * g, x0, xc0, p.cols, r, ny, a_up, a_dn, cK_up,
-                                    cK_dn, tol, o0, o1))
-                    um |= 1u << i;
-                if (vec_ok) {
-                    __stcs(reinterpret_cast<uint2*>(orow + x0), make_uint2(o0, o1));
-                } else {
-                    for (int j = 0; j < 8; ++j) orow[x0 + j] = (uint8_t)((j < 4 ? o0 : o1) >> (8 * (j & 3)));
+                if (!u) um1 &= ~(1u << i);  // every open pixel is below the tighter ceil(t_lo): black, as stored
+            }
+        }
+        // What is left: per-pixel block bounds (each pixel's own clipped count, <= 3 columns of
+        // slack per side), four groups at a time by the whole warp -- lane l takes pixel l & 7 of
+        // the chunk's group l >> 3 and stores its byte when decided.  pm: the lane's pixels still
+        // open after that, one byte per slot, for the exact path.
+        uint32_t pm = 0;
+        if (__any_sync(0xffffffffu, um1 != 0u)) {
+            __syncwarp();  // the owners' provisional stores precede the byte stores below
+#pragma unroll 1
+            for (int i = 0; i < BB_GPL; ++i) {
+                uint32_t bal = __ballot_sync(0xffffffffu, (um1 >> i) & 1u);
+                while (bal) {
+                    const uint32_t src = __fns(bal, 0, (lane >> 3) + 1);  // the chunk's (l >> 3)-th group owner
+                    const int j = lane & 7;
+                    int v = 0x100;  // no pixel
+                    if (src != 0xFFFFFFFFu) {
+                        const int g = (int)src + 32 * i, x = X0 + 8 * g + j;
+                        if (x < p.cols) {
+                            v = bb_pixel_decide(PSe, PQe, F[8 * g + j], alpha + 8 * g + j, x, xc0, p.cols, r, ny,
+                                                a_up, a_dn, cK_up, cK_dn, tol);
+                            if (v >= 0) orow[x] = (uint8_t)v;
+                        }
+                    }
+                    const uint32_t ob = __ballot_sync(0xffffffffu, v < 0);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t sq = __fns(bal, 0, q + 1);
+                        if (sq == (uint32_t)lane) pm |= ((ob >> (8 * q)) & 0xFFu) << (8 * i);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) bal &= bal - 1;  // (0 & -1 stays 0)
                 }
             }
         }
-        if (edge_strip) {
-            // groups whose windows the image's left / right edge clips: per-pixel bounds, the
-            // warp's lanes over their pixels (left groups [0, gl), right groups [gr, ngv))
-            const int nbp = 8 * (gl + ngv - gr);
-            for (int q0 = 0; q0 < nbp; q0 += 64) {  // two pixels per lane per pass (ILP)
-                int v[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int q = q0 + 32 * h + lane;
-                    v[h] = 0x100;  // no pixel
-                    if (q < nbp) {
-                        const int gq = (q >> 3) < gl ? (q >> 3) : gr + (q >> 3) - gl, j = q & 7;
-                        const int x = X0 + 8 * gq + j;
-                        if (x < p.cols)
-                            v[h] = bb_pixel_decide(PSe, PQe, F[8 * gq + j], alpha + 8 * gq + j, x, xc0,
-                                                   p.cols, r, ny, a_up, a_dn, cK_up, cK_dn, tol);
-                    }
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int q = q0 + 32 * h + lane;
-                    const int gq = (q >> 3) < gl ? (q >> 3) : gr + (q >> 3) - gl, j = q & 7;
-                    if (v[h] != 0x100) orow[X0 + 8 * gq + j] = (uint8_t)(v[h] & 0xFF);
-                    unsigned ob = __ballot_sync(0xffffffffu, v[h] < 0);
-                    while (ob) {  // owners of groups with an open pixel
-                        const int qb = q0 + 32 * h + __ffs(ob) - 1;
-                        ob &= ob - 1;
-                        const int gb = (qb >> 3) < gl ? (qb >> 3) : gr + (qb >> 3) - gl;
-                        if ((gb & 31) == lane) um |= 1u << (gb >> 5);
-                    }
-                }
-            }
-            __syncwarp();  // the byte stores above precede an owner's exact rewrite below
-        }
-        // uncertain groups: exact per-pixel re-decision, one group at a time by the warp
-        while (__any_sync(0xffffffffu, um != 0u)) {
-            const unsigned bal = __ballot_sync(0xffffffffu, um != 0u);
+        // pixels still open: exact window sums, one group at a time by the warp
+        while (__any_sync(0xffffffffu, pm != 0u)) {
+            const unsigned bal = __ballot_sync(0xffffffffu, pm != 0u);
             const int src = __ffs(bal) - 1;
-            const int slot = __shfl_sync(0xffffffffu, um ? __ffs(um) - 1 : 0, src);
+            const uint32_t pms = __shfl_sync(0xffffffffu, pm, src);
+            const int slot = (__ffs(pms) - 1) >> 3;
             const int g = src + 32 * slot;
-            const uint2 wv = bb_exact_group<SEG>(&p, in0, PSe, PQe, F, g, y, X0, xc0, alpha, ny);
-            if (tdbg && lane == 0) tdbg[2] += 1;
-            if (lane == src) {
-                um &= ~(1u << slot);
-                const int x0 = X0 + 8 * g;
-                if (vec_ok && x0 + 8 <= p.cols) {
-                    __stcs(reinterpret_cast<uint2*>(orow + x0), wv);
-                } else {
-                    for (int j = 0; j < 8 && x0 + j < p.cols; ++j)
-                        orow[x0 + j] = (uint8_t)((j < 4 ? wv.x : wv.y) >> (8 * (j & 3)));
-                }
-            }
+            bb_exact_pixels<SEG>(&p, in0, PSe, PQe, F, g, y, X0, xc0, alpha, ny, (pms >> (8 * slot)) & 0xFFu, orow);
+            if (tdbg && lane == 0) tdbg[2] = ((tdbg[2] & 0xFFFFull) + 1) | ((unsigned long long)y << 16) | ((unsigned long long)g << 40);
+            if (lane == src) pm &= ~(0xFFu << (8 * slot));
         }
         __syncwarp();  // every lane is done with slot cs and with the prefix planes
         ps = cs;
@@ -924,17 +987,17 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     slide_constants(p);
     int tw;
     if (!bb_geometry(p.r, tw)) return cudaErrorInvalidValue;
-    // Strip plan.  Interior strips output up to tw columns.  The strips holding the image's
-    // left / right edge also decide their edge groups per pixel (~2x the output-side work per
-    // group), so on wide pages they get ~1/5 of a strip (at least 2r columns): with half-width
-    // edge strips those two strips finished last (C4 timeline: 319 vs 282 us mean); the width
-    // sweep 62/50/38/30/20/14/10 % of a strip measured 0.367/0.347/0.342/0.341/0.334/0.340/0.339 ms.
+    // Strip plan.  Interior strips output up to tw columns.  The strips holding the image's left /
+    // right edge run their edge groups (count bounds per group, ~2x the instructions of an
+    // interior group, in a divergent pass of their own) on top of the interior ones, so on wide
+    // pages they are BB_EDGE_PCT % of a strip wide: all pipelines run in one wave and the slowest
+    // strip sets the kernel time.
     int ns, tw0;
     if (p.cols >= 4 * tw) {
 #ifndef BB_EDGE_PCT
-#define BB_EDGE_PCT 20
+#define BB_EDGE_PCT 75
 #endif
-        const int e = std::max(16 * ((2 * p.r + 15) / 16), 16 * ((tw * BB_EDGE_PCT / 100 + 15) / 16));
+        const int e = 16 * ((tw * BB_EDGE_PCT / 100 + 15) / 16);
         const int m = (p.cols - 2 * e + tw - 1) / tw;
         p.TW = 16 * ((p.cols - 2 * e + 16 * m - 1) / (16 * m));
         tw0 = e;
@@ -957,26 +1020,64 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // pairing measured 1.5% slower (0.343 vs 0.337 ms), so tall bands keep separate warm-ups.
     bool paired = true;
     int npairs0 = bb_plan_pairs(rows_out, ns * n_images, num_sms * occ, p.r, true);
-    if ((rows_out + 2 * npairs0 - 1) / (2 * npairs0) >= 2 * p.r + 1) {
+#ifndef BB_PAIR_ALWAYS
+#define BB_PAIR_ALWAYS 0
+#endif
+    if (!BB_PAIR_ALWAYS && (rows_out + 2 * npairs0 - 1) / (2 * npairs0) >= 2 * p.r + 1) {
         paired = false;
         npairs0 = bb_plan_pairs(rows_out, ns * n_images, num_sms * occ, p.r, false);
     }
     p.TH = (rows_out + 2 * npairs0 - 1) / (2 * npairs0);
-    const int nb = (rows_out + p.TH - 1) / p.TH;  // non-empty bands; pair j = bands 2j, 2j+1
-    const int npairs = (nb + 1) / 2;
-    const long long nc = (long long)ns * npairs * n_images;
+    int nb = (rows_out + p.TH - 1) / p.TH;  // non-empty bands; pair j = bands 2j, 2j+1
+    int npairs = (nb + 1) / 2;
+    // One page in one wave of pipelines: the edge strips' rows cost ~BB_EDGE_COST % of an interior
+    // strip's (their edge groups run in a divergent pass of their own, and they refine more), so
+    // they get shorter bands.  Search the interior pair count; the edge strips take the CTA slots
+    // that are left.
+#ifndef BB_EDGE_COST
+#define BB_EDGE_COST 120
+#endif
+    int npairs_e = 0, th_e = 0;
+    const int slots = num_sms * occ;
+    if (ns >= 4 && n_images == 1 && BB_EDGE_COST > 100 && ns * npairs <= slots) {
+        const double wu = (paired ? 0.05 : 0.1) * (2 * p.r + 1), fe = BB_EDGE_COST / 100.0;
+        double best = 1e300;
+        int bi = 0, be = 0;
+        for (int ni = 1; (ns - 2) * ni + 2 <= slots; ++ni) {
+            const int ne = std::min((slots - (ns - 2) * ni) / 2, (rows_out + 1) / 2);
+            const int thi = (rows_out + 2 * ni - 1) / (2 * ni), the = (rows_out + 2 * ne - 1) / (2 * ne);
+            if (paired != (thi < 2 * p.r + 1)) continue;  // keep the warm-up mode planned above
+            const double cost = std::max(thi + wu, fe * (the + wu));
+            if (cost < best) { best = cost; bi = ni; be = ne; }
+        }
+        if (bi > 0) {
+            p.TH = (rows_out + 2 * bi - 1) / (2 * bi);
+            nb = (rows_out + p.TH - 1) / p.TH;
+            npairs = (nb + 1) / 2;
+            th_e = (rows_out + 2 * be - 1) / (2 * be);
+            npairs_e = ((rows_out + th_e - 1) / th_e + 1) / 2;
+        }
+    }
+    const long long nc = npairs_e ? ((long long)(ns - 2) * npairs + 2 * npairs_e) * n_images
+                                  : (long long)ns * npairs * n_images;
     if (nc > 0x7fffffffll) return cudaErrorInvalidValue;
     const int ctas = (int)nc;
     const size_t smem = BB_CTA_BYTES;
     if (print)
-        fprintf(stderr, "[dtb plan] bb_kernel cols=%d rows=%d r=%d strips=%d TW=%d (first %d) bands=%d TH=%d pairs=%d%s ctas=%d occ=%d smem=%zu\n",
-                p.cols, rows_out, p.r, ns, p.TW, tw0, nb, p.TH, npairs, paired ? " (shared warm-up)" : "", ctas, occ, smem);
+        fprintf(stderr, "[dtb plan] bb_kernel cols=%d rows=%d r=%d strips=%d TW=%d (first %d) bands=%d TH=%d pairs=%d%s edge TH=%d pairs=%d ctas=%d occ=%d smem=%zu\n",
+                p.cols, rows_out, p.r, ns, p.TW, tw0, nb, p.TH, npairs, paired ? " (shared warm-up)" : "", th_e, npairs_e, ctas, occ, smem);
     BBMaps mp{};
     e = bb_encode_maps(p, n_images, &mp);
     if (e != cudaSuccess) return e;
     set_last_kernel("bb_kernel");
-    if (p.nseg) bb_kernel<true, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0);
-    else bb_kernel<false, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0);
+    // age skew of the band heights: only when the page fills one wave of tall bands (with fewer
+    // CTAs than slots the schedulers are not contended the same way)
+#ifndef BB_SKEW
+#define BB_SKEW 0
+#endif
+    const int skew = (!paired && ctas * 10 >= slots * 9 && ctas <= slots) ? BB_SKEW : 0;
+    if (p.nseg) bb_kernel<true, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e, skew);
+    else bb_kernel<false, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e, skew);
     return cudaGetLastError();
 }
 

@@ -39,7 +39,9 @@ L.dtb_debug_bb_times(buf.data_ptr(), 16384)
 run()
 torch.cuda.synchronize()
 L.dtb_debug_bb_times(None, 0)
-t = buf.view(-1, 4).cpu().numpy().astype(np.float64)
+traw = buf.view(-1, 4).cpu().numpy()
+t = traw.astype(np.float64)
+t[:, 2] = (traw[:, 2] & 0xFFFF)
 n = int((t[:, 1] > 0).sum())
 t = t[:n]
 t0 = t[:, 0].min()
@@ -56,11 +58,27 @@ print(mode, "kernel ms %.4f" % (e0.elapsed_time(e1) / 10), L.dtb_last_kernel().d
 print(mode, "ctas", n, "span us %.1f" % en.max(), "start max %.1f" % st.max())
 for name, v in (("duration", dur), ("warm-up", warm), ("main", en - wu)):
     print("%-9s us: min %.1f p50 %.1f p90 %.1f max %.1f" % (name, v.min(), np.median(v), np.percentile(v, 90), v.max()))
-ns = int(sys.argv[3]) if len(sys.argv) > 3 else 20
-strip = (np.arange(n) // 2) % ns  # pipelines 2c, 2c+1 share CTA c
+# CTA -> strip (the launch plan: DTB_PLAN="strips pairs edge_pairs", from DTB_PRINT_PLAN=1's line)
+import os
+plan = [int(v) for v in os.environ.get("DTB_PLAN", "20 59 0").split()]
+ns, npairs, npairs_e = plan
+cta = np.arange(n) // 2  # pipelines 2c, 2c+1 share CTA c
+if npairs_e == 0:
+    strip = cta % ns
+    band = 2 * ((cta // ns) % npairs) + (np.arange(n) % 2 == 0)
+else:
+    n_edge = 2 * npairs_e  # the edge strips' CTAs come first
+    strip = np.where(cta < n_edge, np.where(cta % 2 == 1, ns - 1, 0), 1 + (cta - n_edge) % (ns - 2))
+    band = np.where(cta < n_edge, 2 * (cta // 2), 2 * ((cta - n_edge) // (ns - 2))) + (np.arange(n) % 2 == 0)
 for s_ in range(ns):
     m = strip == s_
-    print("strip %2d dur mean %.1f max %.1f  warm mean %.1f  exact %d" % (s_, dur[m].mean(), dur[m].max(), warm[m].mean(), t[m, 2].sum()))
+    print("strip %2d n %4d dur mean %.1f max %.1f  warm mean %.1f  exact %d" % (s_, m.sum(), dur[m].mean(), dur[m].max(), warm[m].mean(), t[m, 2].sum()))
+mi = (strip > 0) & (strip < ns - 1)
+bmax = band[mi].max() + 1
+for q in range(8):
+    m = mi & (band * 8 // bmax == q)
+    if m.any():
+        print("interior bands octile %d: dur mean %.1f p90 %.1f max %.1f exact %d" % (q, dur[m].mean(), np.percentile(dur[m], 90), dur[m].max(), t[m, 2].sum()))
 order = np.argsort(-en)[:8]
 for i in order:
-    print("cta %5d start %.1f warm_end %.1f end %.1f exact %d" % (i, st[i], wu[i], en[i], t[i, 2]))
+    print("cta %5d strip %2d band %3d start %.1f warm_end %.1f end %.1f exact %d last exact y %d g %d" % (i // 2, strip[i], band[i], st[i], wu[i], en[i], t[i, 2], (traw[i, 2] >> 16) & 0xFFFFFF, traw[i, 2] >> 40))
