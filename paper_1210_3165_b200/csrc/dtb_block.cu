@@ -345,7 +345,7 @@ template <bool SEG, int MINB>
 __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ SlideParams p,
                                                       const __grid_constant__ BBMaps mp,
                                                       int nstrips, int npairs, int tw0, int paired,
-                                                      int npairs_e, int th_e, int skew) {
+                                                      int npairs_e, int th_e) {
     constexpr int NS = BB_STAGES, NC = BB_NC, NB = BB_NB, PLW = BB_PLW;
     extern __shared__ __align__(128) uint8_t smb[];
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform for the compiler
@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
     // blockIdx.x -> (strip, band pair, image).  npairs_e > 0: the two edge strips (costlier rows)
     // have their own, shorter bands -- th_e rows, npairs_e pairs -- after the interior strips' CTAs
     int strip, pair, img, TH = p.TH;
+    bool ecls = false;  // a CTA of the edge strips' own band plan
     if (npairs_e == 0) {
         strip = (int)blockIdx.x % nstrips;
         const int rest = (int)blockIdx.x / nstrips;
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             strip = (idx & 1) ? nstrips - 1 : 0;
             pair = idx >> 1;
             TH = th_e;
+            ecls = true;
         } else {
             strip = 1 + (idx - n_edge) % (nstrips - 2);
             pair = (idx - n_edge) / (nstrips - 2);
@@ -391,18 +393,10 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
     const int xc0 = X0 - r - alpha;
     // B = first row of band 2j+1 (or the end of the output rows); warp 0 outputs [B, yb) going
     // down, warp 1 outputs [ya, B) going up
-    // band b of nbc starts at row S(b).  skew == 0: S(b) = b TH.  Otherwise the bands shrink
-    // linearly with the CTA index, from (1 + skew/256) to (1 - skew/256) of the mean height: the
-    // SM's warp schedulers favour older warps, so later CTAs run measurably slower
-    // (C4 timeline: 188 -> 225 us from the first to the last octile of CTAs at equal heights).
-    const int rows_out = p.out_end - p.out_begin;
-    const int nbc = (strip == 0 || strip == nstrips - 1) && npairs_e ? 2 * npairs_e : 2 * npairs;
-    auto S = [&](int b) {
-        if (!skew) return min(p.out_begin + b * TH, p.out_end);
-        if (b >= nbc) return p.out_end;
-        const long long num = (long long)b * (256 + skew) * nbc - (long long)skew * b * b;
-        return p.out_begin + (int)((long long)rows_out * num / (256ll * nbc * nbc));
-    };
+    // band b starts at row S(b) = b TH (clipped to the output rows).  (Band heights skewed by CTA
+    // age -- the warp schedulers favour older warps, C4 timeline 188 -> 225 us from the first to
+    // the last octile of CTAs -- measured no gain: the SM's total issue rate is the bound.)
+    auto S = [&](int b) { return min(p.out_begin + b * TH, p.out_end); };
     const int ya_up = S(2 * pair);
     const int B = S(2 * pair + 1);
     // paired == 0 (tall bands, where the warm-up is a small share): both warps run downward
@@ -1070,14 +1064,8 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     e = bb_encode_maps(p, n_images, &mp);
     if (e != cudaSuccess) return e;
     set_last_kernel("bb_kernel");
-    // age skew of the band heights: only when the page fills one wave of tall bands (with fewer
-    // CTAs than slots the schedulers are not contended the same way)
-#ifndef BB_SKEW
-#define BB_SKEW 0
-#endif
-    const int skew = (!paired && ctas * 10 >= slots * 9 && ctas <= slots) ? BB_SKEW : 0;
-    if (p.nseg) bb_kernel<true, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e, skew);
-    else bb_kernel<false, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e, skew);
+    if (p.nseg) bb_kernel<true, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e);
+    else bb_kernel<false, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e);
     return cudaGetLastError();
 }
 
