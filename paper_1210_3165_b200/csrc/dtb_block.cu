@@ -1017,7 +1017,10 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
 #ifndef BB_PAIR_ALWAYS
 #define BB_PAIR_ALWAYS 0
 #endif
-    if (!BB_PAIR_ALWAYS && (rows_out + 2 * npairs0 - 1) / (2 * npairs0) >= 2 * p.r + 1) {
+#ifndef BB_PAIR_NEVER
+#define BB_PAIR_NEVER 0
+#endif
+    if (BB_PAIR_NEVER || (!BB_PAIR_ALWAYS && (rows_out + 2 * npairs0 - 1) / (2 * npairs0) >= 2 * p.r + 1)) {
         paired = false;
         npairs0 = bb_plan_pairs(rows_out, ns * n_images, num_sms * occ, p.r, false);
     }

@@ -1053,7 +1053,7 @@ cudaError_t set_fp32_audit(unsigned long long* counters) {
 // bb_kernel than on the per-pixel kernels (each pipeline's 2r-row warm-up dominates a short
 // band), break even near r=50 and win from r~57 (W115: 0.113 vs 0.117 ms, W243: 0.140 vs 0.154).
 #ifndef DTB_BB_MIN_R
-#define DTB_BB_MIN_R 56
+#define DTB_BB_MIN_R 32
 #endif
 #ifndef DTB_BB_MIN_R_LARGE
 #define DTB_BB_MIN_R_LARGE 24
