@@ -1048,12 +1048,12 @@ cudaError_t set_fp32_audit(unsigned long long* counters) {
 }
 
 // DTB_BB: 0 never, 1 whenever eligible, 2 (default): eligible and either r >= DTB_BB_MIN_R, or
-// r >= DTB_BB_MIN_R_LARGE on pages of >= 2^26 output pixels.  Measured (profiles/r02_config_table
-// files): C4 (16384^2, r=63) 0.40 vs 0.50 ms; 4096^2 pages at r=9..49 are 1.2-6x slower on
-// bb_kernel than on the per-pixel kernels (each pipeline's 2r-row warm-up dominates a short
-// band), break even near r=50 and win from r~57 (W115: 0.113 vs 0.117 ms, W243: 0.140 vs 0.154).
+// r >= DTB_BB_MIN_R_LARGE on pages of >= 2^26 output pixels.  Measured on the 4096^2 page
+// (scripts/c5_probe.py, round 2c): W59 (r=29) 0.098 ms on either kernel, W63 0.068 vs 0.108 ms,
+// W67 0.078 vs 0.104; at W <= 51 the 13 columns of block slack are too large a share of the window
+// (most groups stay open: W43 0.30 ms, W19 0.40 ms vs 0.09 on the per-pixel kernel).
 #ifndef DTB_BB_MIN_R
-#define DTB_BB_MIN_R 32
+#define DTB_BB_MIN_R 31
 #endif
 #ifndef DTB_BB_MIN_R_LARGE
 #define DTB_BB_MIN_R_LARGE 24
