@@ -1015,7 +1015,7 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     bool paired = true;
     int npairs0 = bb_plan_pairs(rows_out, ns * n_images, num_sms * occ, p.r, true);
 #ifndef BB_PAIR_ALWAYS
-#define BB_PAIR_ALWAYS 0
+#define BB_PAIR_ALWAYS 1
 #endif
 #ifndef BB_PAIR_NEVER
 #define BB_PAIR_NEVER 0
@@ -1032,7 +1032,7 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // they get shorter bands.  Search the interior pair count; the edge strips take the CTA slots
     // that are left.
 #ifndef BB_EDGE_COST
-#define BB_EDGE_COST 120
+#define BB_EDGE_COST 135
 #endif
     int npairs_e = 0, th_e = 0;
     const int slots = num_sms * occ;
@@ -1043,7 +1043,7 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
         for (int ni = 1; (ns - 2) * ni + 2 <= slots; ++ni) {
             const int ne = std::min((slots - (ns - 2) * ni) / 2, (rows_out + 1) / 2);
             const int thi = (rows_out + 2 * ni - 1) / (2 * ni), the = (rows_out + 2 * ne - 1) / (2 * ne);
-            if (paired != (thi < 2 * p.r + 1)) continue;  // keep the warm-up mode planned above
+            if (!BB_PAIR_ALWAYS && !BB_PAIR_NEVER && paired != (thi < 2 * p.r + 1)) continue;  // keep the warm-up mode planned above
             const double cost = std::max(thi + wu, fe * (the + wu));
             if (cost < best) { best = cost; bi = ni; be = ne; }
         }
