@@ -60,6 +60,9 @@ namespace dtb {
 #ifndef BB_STAGES
 #define BB_STAGES 3  // ring depth per warp (the warp refills a slot right after consuming it)
 #endif
+#ifndef BB_MINB
+#define BB_MINB 8  // resident CTAs (pipeline pairs) per SM the register budget is set for
+#endif
 #ifndef BB_GPL
 #define BB_GPL (BB_NC_DEF / 256)  // group slots per lane (groups of 8 output columns)
 #endif
@@ -1006,7 +1009,7 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     int occ = 1;
-    e = p.nseg ? bb_prepare<true, 8>(dev, &occ) : bb_prepare<false, 8>(dev, &occ);
+    e = p.nseg ? bb_prepare<true, BB_MINB>(dev, &occ) : bb_prepare<false, BB_MINB>(dev, &occ);
     if (e != cudaSuccess) return e;
     const int rows_out = p.out_end - p.out_begin;
     // Pair the bands (shared warm-up, one band running upward) when the bands come out shorter
@@ -1067,8 +1070,8 @@ cudaError_t launch_block(SlideParams p, int n_images, int num_sms, cudaStream_t 
     e = bb_encode_maps(p, n_images, &mp);
     if (e != cudaSuccess) return e;
     set_last_kernel("bb_kernel");
-    if (p.nseg) bb_kernel<true, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e);
-    else bb_kernel<false, 8><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e);
+    if (p.nseg) bb_kernel<true, BB_MINB><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e);
+    else bb_kernel<false, BB_MINB><<<ctas, 64, smem, st>>>(p, mp, ns, npairs, tw0, paired ? 1 : 0, npairs_e, th_e);
     return cudaGetLastError();
 }
 

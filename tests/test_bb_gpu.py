@@ -88,6 +88,16 @@ def test_narrow_images():
         _check(img, win, 0.34)
 
 
+def test_lanes_with_two_edge_groups():
+    # left- and right-edge groups 32 slots apart land in the same lane: the first one's count
+    # bounds come packed from the prologue, the second one's are derived in the row loop
+    for w, win in ((330, 127), (333, 127), (700, 249), (523, 191)):
+        img = workloads.doc_gray(140, w, w % 13 + 1, 70)
+        _check(img, win, 0.34)
+        # low contrast, t ~ 0.87 m: bounds leave many groups open -> refinement and exact path
+        _check((img // 4 + 90).astype(np.uint8), win, 0.15)
+
+
 def test_right_edge_partial_strip():
     for w in (912, 1808, 2128, 4112, 16384):
         img = workloads.doc_gray(150, w, w, 300)
@@ -199,9 +209,9 @@ def test_band_pair_counts(h):
     _check(img, 63, 0.34)
 
 
-def test_tall_bands_unpaired_and_short_bands_paired():
-    # a tall page plans bands taller than W (separate warm-ups), a short one shorter (shared);
-    # both parities against the oracle
+def test_tall_and_short_bands():
+    # bands taller and shorter than the window (both share the pair's warm-up); both parities
+    # against the oracle
     for h, w in ((1400, 41), (300, 201)):
         img = workloads.doc_gray(h, 3000, 5, 1400 + h)
         _check(img, w, 0.34)
