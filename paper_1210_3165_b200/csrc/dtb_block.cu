@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
         // open after that, one byte per slot, for the exact path.
         uint32_t pm = 0;
         if (__any_sync(0xffffffffu, um1 != 0u)) {
+            BB_PERTURB(pid, 4 * k + 2);
             __syncwarp();  // the owners' provisional stores precede the byte stores below
 #pragma unroll 1
             for (int i = 0; i < BB_GPL; ++i) {
@@ -826,6 +827,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             }
         }
         // pixels still open: exact window sums, one group at a time by the warp
+        BB_PERTURB(pid, 4 * k + 3);
         while (__any_sync(0xffffffffu, pm != 0u)) {
             const unsigned bal = __ballot_sync(0xffffffffu, pm != 0u);
             const int src = __ffs(bal) - 1;
