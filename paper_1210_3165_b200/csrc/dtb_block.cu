@@ -553,6 +553,21 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
         __syncwarp();
     };
 
+    // the same for a row item of the row loop (row y staged at st; fst: only the centre row)
+    auto rag_patch_row = [&](int y, bool fst, uint8_t* st) {
+        const int nt = p.cols - cols8;
+        if (lane < 3 * 8) {
+            const int w = lane >> 3, b = lane & 7;
+            int g = -1, off = cols8 - xc0;
+            if (w == 0 && !fst) g = y + d * r;
+            if (w == 1 && !fst) g = y - d * (r + 1);
+            if (g >= p.H) g = -1;
+            if (w == 2) { g = y; off = cols8 - X0; }
+            if (g >= 0 && b < nt && off + b >= 0 && off + b < NC) st[w * NC + off + b] = row_at<SEG>(p, in0, g)[cols8 + b];
+        }
+        __syncwarp();
+    };
+
     // ---- ring fill, then the warm-up items (block sums of the initial window).  cs / cph: the
     // consumer's slot and phase parity; ps: the slot the previous item left, refilled with item
     // k + NS - 1 at the top of iteration k.
@@ -586,32 +601,48 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
     if (pr) bb_exchange(xbuf, warp, lane, bS, bQ);
     if (tdbg && lane == 0) tdbg[3] = bb_gtimer();
 
-    // ---- row items
+    // ---- row items.  The loop's bookkeeping is explicit shared-window addresses and byte
+    // offsets stepped by constants (slot indices would cost a multiply and an address conversion
+    // per use: ~45 uniform-datapath instructions per row in the round-2d profile).
     const int dr = d * r, dr1 = d * (r + 1);
     const int64_t dpitch = (int64_t)d * p.bin_pitch;
     uint8_t* orow = obase + (int64_t)ystart * p.bin_pitch;
     const uint8_t* lcol = ring + 4 * BB_BPL * lane;  // this lane's 32 bytes of a staged row
-    int y = ystart;
-    for (int k = nwarm; k < n_items; ++k, y += d, orow += dpitch) {
-        if (k + NS - 1 < n_items) {
-            // item k+NS-1 is a plain row item here (never the warm-up-covered first row)
-            BB_PERTURB(pid, 4 * (k + NS - 1));
-            uint8_t* E = ring + ps * 3 * NC;
-            const int y2 = y + d * (NS - 1);
+    const uint32_t ring_a = smem_u32(ring), full_a = smem_u32(full);
+    uint32_t coff = (uint32_t)cs * 3u * NC, cbar = full_a + 8u * (uint32_t)cs;  // consumer's slot
+    uint32_t poff = (uint32_t)ps * 3u * NC, pbar = full_a + 8u * (uint32_t)ps;  // slot to refill
+    bool fst = d > 0;                   // the downward band's first row: covered by the warm-up
+    int y = ystart, yt = ystart + d * (NS - 1);  // yt: the row staged at the top of the iteration
+    for (int left = n_items - nwarm; left > 0; --left, y += d, yt += d, orow += dpitch) {
+        if (left > NS - 1) {
+            // the item NS-1 rows ahead is a plain row item (never the warm-up-covered first row)
+            BB_PERTURB(pid, 4 * left);
             if (bb_elect()) {
                 if (rag) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&full[ps], 3 * NC);
-                stage_row(E, x8E, y2 + dr, &full[ps], pol_E);
-                stage_row(E + NC, x8E, y2 - dr1, &full[ps], pol_O);
-                stage_row(E + 2 * NC, x8F, y2, &full[ps], pol_F);
+                mbar_expect_tx_a(pbar, 3 * NC);
+                const uint32_t E = ring_a + poff;
+                if (SEG) {
+                    const int gE = yt + dr, gO = yt - dr1;
+                    const int iE = gE >= p.seg_lo[2] ? 2 : (gE >= p.seg_lo[1] ? 1 : 0);
+                    const int iO = gO >= p.seg_lo[2] ? 2 : (gO >= p.seg_lo[1] ? 1 : 0);
+                    const int iF = yt >= p.seg_lo[2] ? 2 : (yt >= p.seg_lo[1] ? 1 : 0);
+                    tma_load_3d_a(E, &mp.m[iE], x8E, gE - p.seg_lo[iE], 0, pbar, pol_E);
+                    tma_load_3d_a(E + NC, &mp.m[iO], x8E, gO - p.seg_lo[iO], 0, pbar, pol_O);
+                    tma_load_3d_a(E + 2 * NC, &mp.m[iF], x8F, yt - p.seg_lo[iF], 0, pbar, pol_F);
+                } else {
+                    const int yb = yt - p.row0;
+                    tma_load_3d_a(E, &mp.m[0], x8E, yb + dr, img, pbar, pol_E);
+                    tma_load_3d_a(E + NC, &mp.m[0], x8E, yb - dr1, img, pbar, pol_O);
+                    tma_load_3d_a(E + 2 * NC, &mp.m[0], x8F, yb, img, pbar, pol_F);
+                }
             }
         }
-        mbar_wait(&full[cs], cph);
-        BB_PERTURB(pid, 4 * k + 1);
-        if (rag) rag_patch(k, cs);
-        const int soff = cs * 3 * NC;
+        mbar_wait_a(cbar, cph);
+        BB_PERTURB(pid, 4 * left + 1);
+        const int soff = (int)coff;
+        if (rag) rag_patch_row(y, fst, ring + soff);
         // ---- column side: block sums, exclusive block prefix -> even / odd planes
-        if (!(k == nwarm && d > 0)) {
+        if (!fst) {
             const uint4* E = reinterpret_cast<const uint4*>(lcol + soff);
             const uint4* O = reinterpret_cast<const uint4*>(lcol + soff + NC);
 #pragma unroll
@@ -633,7 +664,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             uint32_t iS = TS, iQ = TQ;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) bb_scan_step(iS, iQ, off);
-            BB_PERTURB(pid, 4 * k + 2);
+            BB_PERTURB(pid, 4 * left + 2);
             // lane's exclusive prefix P[16 lane + j]: even j -> even plane, odd j -> odd plane
             uint32_t vS = iS - TS, vQ = iQ - TQ;
 #pragma unroll
@@ -658,7 +689,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             }
         }
         __syncwarp();
-        BB_PERTURB(pid, 4 * k + 3);
+        BB_PERTURB(pid, 4 * left + 3);
         // ---- output side: groups of 8 pixels
         const uint8_t* F = ring + soff + 2 * NC;
         const int ny = min(y + r, p.H - 1) - max(y - r, 0) + 1;
@@ -798,7 +829,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
         // open after that, one byte per slot, for the exact path.
         uint32_t pm = 0;
         if (__any_sync(0xffffffffu, um1 != 0u)) {
-            BB_PERTURB(pid, 4 * k + 2);
+            BB_PERTURB(pid, 4 * left + 2);
             __syncwarp();  // the owners' provisional stores precede the byte stores below
 #pragma unroll 1
             for (int i = 0; i < BB_GPL; ++i) {
@@ -827,7 +858,7 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             }
         }
         // pixels still open: exact window sums, one group at a time by the warp
-        BB_PERTURB(pid, 4 * k + 3);
+        BB_PERTURB(pid, 4 * left + 3);
         while (__any_sync(0xffffffffu, pm != 0u)) {
             const unsigned bal = __ballot_sync(0xffffffffu, pm != 0u);
             const int src = __ffs(bal) - 1;
@@ -838,9 +869,13 @@ __global__ void __launch_bounds__(64, MINB) bb_kernel(const __grid_constant__ Sl
             if (tdbg && lane == 0) tdbg[2] = ((tdbg[2] & 0xFFFFull) + 1) | ((unsigned long long)y << 16) | ((unsigned long long)g << 40);
             if (lane == src) pm &= ~(0xFFu << (8 * slot));
         }
-        __syncwarp();  // every lane is done with slot cs and with the prefix planes
-        ps = cs;
-        if (++cs == NS) { cs = 0; cph ^= 1u; }
+        __syncwarp();  // every lane is done with the slot and with the prefix planes
+        fst = false;
+        poff = coff;
+        pbar = cbar;
+        coff += 3u * NC;
+        cbar += 8u;
+        if (coff == (uint32_t)NS * 3u * NC) { coff = 0; cbar = full_a; cph ^= 1u; }
     }
     if (tdbg && lane == 0) tdbg[1] = bb_gtimer();
 }

@@ -8,4 +8,4 @@ timeout 300 python bench.py --emulate-bands 8 --steps 10 --warmup 3 2>&1 | tail 
 if [ "${AB_NCU:-0}" = 1 ]; then
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:bb_kernel -c 1 python scripts/bb_probe.py c4 127 2>&1 | grep -E "duration|bytes|hit_rate|inst_exec|issue_active" | awk '{print "   ", $1, $(NF-1), $NF}'
 fi
-[ $# -gt 0 ] && bash scripts/ab_build_probe.sh "$@"
+if [ $# -gt 0 ]; then bash scripts/ab_build_probe.sh "$@"; fi
