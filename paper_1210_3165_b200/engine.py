@@ -115,16 +115,20 @@ def to_device(arr, ndim: int = 2, what: str = "image"):
 
 @_on_input_device
 def binarize(gray, win: int, method: str, k: float, r: float, want_tmap: bool = True,
-             stream=None, out=None):
-    """Whole-image binarize -> (binary uint8 tensor, tmap float64 tensor or None)."""
+             stream=None, out=None, tmap_out=None):
+    """Whole-image binarize -> (binary uint8 tensor, tmap float64 tensor or None).  ``out`` /
+    ``tmap_out``: caller-owned result buffers (steady-state callers reuse them; ``tmap_out`` is
+    an (h, w) float64 view, ideally of a buffer whose row pitch is a multiple of 16 bytes)."""
     torch = torch_mod()
     g = to_device(gray)
     h, w = g.shape
     if out is None:
         out = torch.empty((h, w), dtype=torch.uint8, device=g.device)
     # a 16-byte row pitch lets the fast kernel's paired fp64 stores take the map
-    tmap = (torch.empty((h, w + (w & 1)), dtype=torch.float64, device=g.device)[:, :w]
-            if want_tmap else None)
+    tmap = None
+    if want_tmap:
+        tmap = tmap_out if tmap_out is not None else \
+            torch.empty((h, w + (w & 1)), dtype=torch.float64, device=g.device)[:, :w]
     rc = _lib.lib().dtb_binarize(
         g.data_ptr(), g.stride(0), h, w, 0, h, 0, h, out.data_ptr(), out.stride(0),
         tmap.data_ptr() if tmap is not None else None, (tmap.stride(0) * 8) if tmap is not None else 0,
