@@ -20,6 +20,7 @@ DTB_E_CUDA = -2
 DTB_E_UNSUPPORTED = -3
 
 _c_i32, _c_i64, _c_f64, _c_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+_c_u64 = ctypes.c_uint64
 
 # name -> argtypes, mirroring include/docthresh_b200.h one for one.
 SIGNATURES = {
@@ -54,6 +55,7 @@ SIGNATURES = {
     "dtb_last_kernel": [],
     "dtb_debug_bb_exact": [_c_p, _c_i32],
     "dtb_debug_bb_times": [_c_p, _c_i32],
+    "dtb_debug_sqrt_selftest": [_c_u64, _c_u64, _c_p],
     "dtb_confusion": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
     "dtb_sweep_counts": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_p,
                          _c_i32, _c_i32, _c_f64, _c_p, _c_p],

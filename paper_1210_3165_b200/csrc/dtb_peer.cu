@@ -100,6 +100,47 @@ int dtb_debug_bb_times(uint64_t* device_buf, int32_t cap) {
     return e == cudaSuccess ? DTB_OK : cuda_fail(e, "dtb_debug_bb_times");
 }
 
+// sqrt_rn_pos vs __dsqrt_rn, bit for bit: `count` values per class -- uniform bit patterns with
+// exponents in [-70, 17], and variances formed like the epilogue's (Q/n - (S/n)^2 from integers)
+__global__ void sqrt_selftest_kernel(unsigned long long seed, unsigned long long count,
+                                     unsigned long long* mismatches) {
+    unsigned long long x = seed ^ (0x9E3779B97F4A7C15ull * (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x + 1));
+    unsigned long long bad = 0;
+    const unsigned long long per = (count + (unsigned long long)gridDim.x * blockDim.x - 1) /
+                                   ((unsigned long long)gridDim.x * blockDim.x);
+    for (unsigned long long i = 0; i < per; ++i) {
+        x ^= x << 13; x ^= x >> 7; x ^= x << 17;  // xorshift64
+        const int e = 1023 - 70 + (int)((x >> 52) % 88);
+        const double a = __longlong_as_double(((long long)e << 52) | (long long)(x & 0xFFFFFFFFFFFFFull));
+        if (__double_as_longlong(dtb::sqrt_rn_pos(a)) != __double_as_longlong(__dsqrt_rn(a))) ++bad;
+        x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+        const unsigned n = 9 + (unsigned)(x % 65017);               // window counts 9 .. 255^2
+        const unsigned f0 = (unsigned)((x >> 20) & 255), sp = (unsigned)((x >> 28) & 63);
+        const unsigned long long S = (unsigned long long)n * f0 + ((x >> 34) % (1 + (unsigned long long)n * min(sp, 255u - f0)));
+        const unsigned long long Q = S * f0 + ((x >> 40) % (1 + S * (sp + 1)));
+        const double nd = (double)n, mean = __ddiv_rn((double)S, nd);
+        const double var = __dsub_rn(__ddiv_rn((double)Q, nd), __dmul_rn(mean, mean));
+        if (var > 0.0 && __double_as_longlong(dtb::sqrt_rn_pos(var)) != __double_as_longlong(__dsqrt_rn(var))) ++bad;
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
+int dtb_debug_sqrt_selftest(uint64_t seed, uint64_t count, uint64_t* mismatches) {
+    if (!mismatches) return fail(DTB_E_INVALID, "dtb_debug_sqrt_selftest: mismatches is NULL");
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(*d));
+    if (e == cudaSuccess) e = cudaMemset(d, 0, sizeof(*d));
+    if (e == cudaSuccess) {
+        sqrt_selftest_kernel<<<1184, 256>>>(seed, count, d);
+        e = cudaGetLastError();
+    }
+    unsigned long long h = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    if (d) cudaFree(d);
+    *mismatches = h;
+    return e == cudaSuccess ? DTB_OK : cuda_fail(e, "dtb_debug_sqrt_selftest");
+}
+
 int dtb_debug_bb_exact(uint64_t* count, int32_t reset) {
     if (!count) return fail(DTB_E_INVALID, "null pointer");
     unsigned long long v = 0;

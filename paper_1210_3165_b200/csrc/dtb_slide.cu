@@ -210,7 +210,7 @@ __device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t*
 
 // TMAP variant of row_outputs: every pixel runs the reference fp64 epilogue (t_exact_fast,
 // bit-exact), its threshold goes to the fp64 map row trow[0..V) and its byte to ow.
-template <int V, int RXM4, bool BORDER>
+template <int V, int RXM4, int METHOD, bool BORDER, bool RP2>
 __device__ __forceinline__ void row_outputs_tmap(const uint32_t* sPS, const uint32_t* sPQ,
                                                  const int (&aw)[V / 4 + 1], const int (&bw)[V / 4 + 1],
                                                  const uint8_t* fsm, uint32_t (&ow)[V / 4], double* trow,
@@ -261,7 +261,7 @@ __device__ __forceinline__ void row_outputs_tmap(const uint32_t* sPS, const uint
                 n = (uint32_t)(ny * (min(x + r, cols - 1) - max(x - r, 0) + 1));
                 if (n != p.N) rn = __drcp_rn((double)n);
             }
-            const double t = t_exact_fast(S8[j], Q8[j], n, rn, p.method, p.k, p.rr, rinv);
+            const double t = t_exact_fast<RP2>(S8[j], Q8[j], n, rn, METHOD, p.k, p.rr, rinv);
             t8[j] = t;
             if (!((double)f < t)) bytes[j >> 2] |= 0xFFu << (8 * (j & 3));
         }
@@ -546,12 +546,18 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
             if constexpr (TMAP) {
                 double* trow = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(p.tmap) +
                                                          (y - p.out_begin) * p.tmap_pitch) + xo;
-                if (y_interior && !x_border_warp)
-                    row_outputs_tmap<V, RXM4, false>(sPS, sPQ, aw, bw, fsm, ow, trow, xo, p.cols, ny,
-                                                     p.r, p, rnN, rinv);
-                else
-                    row_outputs_tmap<V, RXM4, true>(sPS, sPQ, aw, bw, fsm, ow, trow, xo, p.cols, ny,
-                                                    p.r, p, rnN, rinv);
+                // (uniform) R a power of two: the interior variant is then free of branches
+                if (y_interior && !x_border_warp) {
+                    if (rinv != 0.0)
+                        row_outputs_tmap<V, RXM4, METHOD, false, true>(sPS, sPQ, aw, bw, fsm, ow, trow, xo, p.cols, ny,
+                                                               p.r, p, rnN, rinv);
+                    else
+                        row_outputs_tmap<V, RXM4, METHOD, false, false>(sPS, sPQ, aw, bw, fsm, ow, trow, xo, p.cols, ny,
+                                                                p.r, p, rnN, rinv);
+                } else {
+                    row_outputs_tmap<V, RXM4, METHOD, true, false>(sPS, sPQ, aw, bw, fsm, ow, trow, xo, p.cols, ny,
+                                                           p.r, p, rnN, rinv);
+                }
             } else if (y_interior && !x_border_warp)
                 unc = row_outputs<V, RXM4, METHOD, false>(sPS, sPQ, aw, bw, fsm, ow, xo, p.cols, ny,
                                                           p.r, p);

@@ -61,7 +61,8 @@ def _header_prototypes():
 
 def test_python_signature_types_match_header():
     """Every ctypes argtype agrees with the C prototype (pointer / int64 / int32 / double)."""
-    want = {"int64_t": ctypes.c_int64, "int32_t": ctypes.c_int32, "double": ctypes.c_double}
+    want = {"int64_t": ctypes.c_int64, "int32_t": ctypes.c_int32, "double": ctypes.c_double,
+            "uint64_t": ctypes.c_uint64}
     protos = _header_prototypes()
     assert set(protos) == set(_lib.SIGNATURES)
     for name, args in protos.items():
