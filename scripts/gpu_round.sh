@@ -10,6 +10,8 @@ timeout 1200 python -m pytest tests -m gpu -x -q > $O/${TAG}_pytest_gpu.log 2>&1
 timeout 600 python bench.py > $O/${TAG}_bench.log 2>&1; echo bench=$?
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/${TAG}_bench_ref.log 2>&1; echo ref=$?
 timeout 600 python bench.py --emulate-bands 8 --steps 10 --warmup 3 > $O/${TAG}_emul8.log 2>&1; echo emul=$?
+timeout 300 python scripts/tmap_probe.py > $O/${TAG}_tmap_probe.log 2>&1; echo tmap=$?
+timeout 300 python scripts/c3_probe.py > $O/${TAG}_c3_probe.log 2>&1; echo c3=$?
 timeout 900 python scripts/config_table.py --reps 10 > $O/${TAG}_config_table.json 2> $O/${TAG}_config_table.err; echo table=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/${TAG}_launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_ncu_launch.log 2>&1; echo launches=$?
