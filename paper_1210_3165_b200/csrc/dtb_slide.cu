@@ -168,12 +168,12 @@ __device__ __forceinline__ bool row_outputs(const uint32_t* sPS, const uint32_t*
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 if (q < 2 || MA) {
-                    DTB_CHECK(aw[2 * g + q] >= 0 && aw[2 * g + q] + 4 <= slide_padded_words(p.NC));
+                    DTB_CHECK(aw[2 * g + q] >= 0 && aw[2 * g + q] + 4 <= slide_padded_words(p.PL));
                     const uint4 v = *reinterpret_cast<const uint4*>(sp + aw[2 * g + q]);
                     A[4 * q] = v.x; A[4 * q + 1] = v.y; A[4 * q + 2] = v.z; A[4 * q + 3] = v.w;
                 }
                 if (q < 2 || MB) {
-                    DTB_CHECK(bw[2 * g + q] >= 0 && bw[2 * g + q] + 4 <= slide_padded_words(p.NC));
+                    DTB_CHECK(bw[2 * g + q] >= 0 && bw[2 * g + q] + 4 <= slide_padded_words(p.PL));
                     const uint4 v = *reinterpret_cast<const uint4*>(sp + bw[2 * g + q]);
                     B[4 * q] = v.x; B[4 * q + 1] = v.y; B[4 * q + 2] = v.z; B[4 * q + 3] = v.w;
                 }
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     constexpr int MB = (RXM4 + 1) & 3;
     constexpr int NS = SLIDE_STAGES;
     extern __shared__ __align__(128) uint32_t sm[];
-    const int NCp = slide_padded_words(p.NC);
+    const int NCp = slide_padded_words(p.PL);
     uint32_t* sPS = sm;
     uint32_t* sPQ = sm + NCp;
     uint32_t* sWS = sm + 2 * NCp;  // per-warp totals (8 + 8 words)
@@ -307,8 +307,13 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint8_t* in = p.in + (int64_t)blockIdx.z * p.img_stride;
     const int X0 = (int)blockIdx.x * p.TW;
-    const int alpha = (16 - (p.rx & 15)) & 15;
-    const int xc0 = X0 - p.rx - alpha;
+    // word RA = alpha + (x - X0) of a prefix array holds P(x - rx - 1), word RA + 2rx + 1 holds
+    // P(x + rx).  Halo layout: column index 0 is image column X0 - rx - alpha.  Edge-padded
+    // layout (p.pad > 0, one strip): column index 0 is image column X0 = 0 and the column threads
+    // write their prefix p.pad words further right.
+    const int alpha = p.pad ? p.pad - p.rx : (16 - (p.rx & 15)) & 15;
+    const int xc0 = p.pad ? X0 : X0 - p.rx - alpha;
+    const int padc = p.pad >> 2;  // chunks
     const int ya = p.out_begin + (int)blockIdx.y * p.TH;
     const int yb = min(ya + p.TH, p.out_end);
     if (ya >= yb) return;
@@ -333,6 +338,11 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
         uint4* r4 = reinterpret_cast<uint4*>(ring);
         const int n16 = NS * 3 * p.NC / 16;
         for (int i = t; i < n16; i += blockDim.x) r4[i] = make_uint4(0, 0, 0, 0);
+        // edge-padded layout: P of the columns left of the image is zero
+        for (int L = t; L < padc; L += blockDim.x) {
+            *reinterpret_cast<uint4*>(&sPS[pchunk_word(L)]) = make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(&sPQ[pchunk_word(L)]) = make_uint4(0, 0, 0, 0);
+        }
     }
     if (t == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -397,9 +407,9 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
     uint32_t qS[4] = {0, 0, 0, 0}, qQ[4] = {0, 0, 0, 0};
 
     const int xo = X0 + V * t;  // this thread's V output columns
-    const bool has_out = (V * t + V + 2 * p.rx + alpha <= p.NC) && (V * t < p.TW) &&
+    const bool has_out = (p.pad || V * t + V + 2 * p.rx + alpha <= p.NC) && (V * t < p.TW) &&
                          (xo < p.cols);
-    const bool out_full = has_out && (xo + 32 <= p.cols) &&
+    const bool out_full = has_out && (xo + V <= p.cols) &&
                           ((reinterpret_cast<uintptr_t>(p.bin) | (uintptr_t)p.bin_pitch |
                             (uintptr_t)p.out_stride) & 15) == 0;
     const bool x_interior = (p.rx == p.r) && (xo - p.r >= 0) && (xo + V - 1 + p.r <= p.cols - 1);
@@ -522,13 +532,24 @@ __global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlidePara
                 cbS[h] += cS[c0 + 2]; cbQ[h] += cQ[c0 + 2];
                 vs.w = cbS[h]; vq.w = cbQ[h];
                 cbS[h] += cS[c0 + 3]; cbQ[h] += cQ[c0 + 3];
-                const int pw = pchunk_word((V / 4) * t + c0 / 4);
+                const int pw = pchunk_word(padc + (V / 4) * t + c0 / 4);
                 DTB_CHECK(pw >= 0 && pw + 4 <= NCp);
                 *reinterpret_cast<uint4*>(&sPS[pw]) = vs;
                 *reinterpret_cast<uint4*>(&sPQ[pw]) = vq;
             }
         }
-        if (t == blockDim.x - 1) {  // logical word NC = P[NC - 1]
+        if (p.pad) {
+            // the row total, repeated over the padr words right of the strip (last warp)
+            if (warp == nwarps - 1) {
+                const uint32_t tS = __shfl_sync(0xffffffffu, bS, 31), tQ = __shfl_sync(0xffffffffu, bQ, 31);
+                for (int L = lane; L < (p.padr >> 2); L += 32) {
+                    const int pw = pchunk_word(padc + p.NC / 4 + L);
+                    DTB_CHECK(pw >= 0 && pw + 4 <= NCp);
+                    *reinterpret_cast<uint4*>(&sPS[pw]) = make_uint4(tS, tS, tS, tS);
+                    *reinterpret_cast<uint4*>(&sPQ[pw]) = make_uint4(tQ, tQ, tQ, tQ);
+                }
+            }
+        } else if (t == blockDim.x - 1) {  // logical word NC = P[NC - 1]
             const int pw = pchunk_word(p.NC / 4);
             sPS[pw] = bS;
             sPQ[pw] = bQ;
@@ -1064,6 +1085,12 @@ cudaError_t set_fp32_audit(unsigned long long* counters) {
 #ifndef DTB_BB_MIN_R_LARGE
 #define DTB_BB_MIN_R_LARGE 24
 #endif
+// DTB_PAD: 0 never, 1 whenever the image fits one strip, 2 (default) when it also saves >= 10%
+// of the column work (read per launch: tests switch it)
+static int pad_mode() {
+    const char* e = getenv("DTB_PAD");
+    return e ? atoi(e) : 2;
+}
 static int bb_mode() {  // read per launch (tests switch it)
     const char* e = getenv("DTB_BB");
     return e ? atoi(e) : 2;
@@ -1116,12 +1143,29 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     }
     Plan pl = plan_for(V);
     int best_w = pl.w, best_strips = pl.strips, best_tw = pl.tw;
+    p.pad = p.padr = 0;
+    // Edge-padded single strip (slide_kernel): an image no wider than one strip needs no halo
+    // columns at all -- its left and right halos lie outside the image.  Taken when that cuts the
+    // column work by >= 10% (C3, 2048 wide, W31: 5 strips x 512 columns -> one of 2048).
+    if (!p.nseg && pad_mode()) {
+        // V = 16 only: 32 columns per thread measured slower on every page that fits (C3 0.712 vs
+        // 0.672 ms, C2 W15 0.136 vs 0.048 ms; scripts/pad_probe.py)
+        const int Vp = 16;
+        const int wp = (p.cols + 32 * Vp - 1) / (32 * Vp);
+        const long workp = 32L * Vp * wp;
+        if (wp <= 8 && (pad_mode() == 1 || best_w == 0 || workp * 10 <= pl.work * 9)) {
+            V = Vp;
+            p.pad = 32 * ((p.rx + 31) / 32);
+            p.padr = 4 * ((p.rx + 4) / 4 + 1);
+            best_w = wp; best_strips = 1; best_tw = 32 * ((p.cols + 31) / 32);
+        }
+    }
     if (best_w == 0) return cudaErrorInvalidValue;  // window too wide for 8 warps (caller checks)
     // Auto V: 16 columns per thread give strips in 512-column steps (and 128-register warps);
     // take them when that cuts the staged column work by >= 10% (C2 pages 2480 wide: one strip
     // of 2560 instead of three of 1024 -- W15 0.119 -> 0.058 ms; C5 W3: 0.093 -> 0.078 ms;
     // C5 W67 / W131 within 2%).
-    if (!p.nseg && !p.tmap && V == 32) {
+    if (!p.nseg && !p.tmap && V == 32 && !p.pad) {
         const Plan p16 = plan_for(16);
         if (p16.w > 0 && p16.work * 10 <= pl.work * 9) {
             V = 16;
@@ -1131,7 +1175,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     // warp-specialized kernel when the strip has >= 2 column warps (measured: C4 0.624 vs 0.656
     // ms; single-column-warp strips such as C3's are faster on the classic kernel)
     const int ws_mode = use_ws();
-    if (V == 32 && (ws_mode == 1 || (ws_mode == 2 && best_w >= 2))) {
+    if (V == 32 && !p.pad && (ws_mode == 1 || (ws_mode == 2 && best_w >= 2))) {
         p.ncw = best_w;
         p.now = (best_tw + 32 * 32 - 1) / (32 * 32);
         p.NC = 1024 * best_w;
@@ -1157,8 +1201,9 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     const int nt = 32 * best_w;
     p.NC = V * nt;
     p.TW = best_tw;
+    p.PL = p.pad ? p.pad + p.NC + p.padr + 16 : p.NC;
     const int nstrips = best_strips;
-    const size_t smem = slide_smem_bytes(p.NC);
+    const size_t smem = slide_smem_bytes(p.NC, p.PL);
     const int m = p.rx & 3;
     const bool sv = p.method == DTB_METHOD_SAUVOLA;
     int occ = 1;
@@ -1171,8 +1216,8 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
     p.TH = (rows_out + nbands - 1) / nbands;
     dim3 grid(nstrips, (rows_out + p.TH - 1) / p.TH, n_images);
     if (print_plan())
-        fprintf(stderr, "[dtb plan] slide_kernel V=%d cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d\n",
-                V, p.cols, rows_out, p.r, best_w, nstrips, best_tw, occ, (int)grid.y, p.TH);
+        fprintf(stderr, "[dtb plan] slide_kernel V=%d cols=%d rows=%d r=%d w=%d strips=%d TW=%d occ=%d bands=%d TH=%d pad=%d\n",
+                V, p.cols, rows_out, p.r, best_w, nstrips, best_tw, occ, (int)grid.y, p.TH, p.pad);
     g_last_kernel = "slide_kernel";
     return V == 16 ? dispatch_rx<16>(m, sv, grid, nt, smem, p, st, nullptr)
                    : dispatch_rx<32>(m, sv, grid, nt, smem, p, st, nullptr);

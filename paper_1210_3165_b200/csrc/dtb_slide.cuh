@@ -25,6 +25,13 @@ struct SlideParams {
     float a, c;        // Sauvola: 1-k, k/R; Niblack: 1, k (border constants are rebuilt per n)
     int l2hint;        // 1: evict_last / evict_first L2 policies on the staged row copies
     int ncw, now;      // warp-specialized kernel: column warps, output warps
+    // slide_kernel, edge-padded single strip (pad > 0): the strip's NC columns are the image
+    // columns [0, NC) themselves -- no halo columns are staged or summed.  The prefix array is
+    // shifted right by `pad` words (= rx + alpha, a multiple of 32); the pad on the left stays
+    // zero (P of a negative column) and `padr` words on the right repeat the row total (P of a
+    // column past the image), so the output side reads both runs exactly as in the halo layout.
+    int pad, padr;
+    int PL;            // logical words of one prefix array (NC, or NC + pad + padr), set by launch_slide
     // Optional segmented input (dtb_binarize_segments): global rows [seg_lo[i], seg_lo[i+1]) live
     // at seg_ptr[i] with pitch seg_pitch[i] -- e.g. a neighbour GPU's halo rows read in place
     // over NVLink (peer / IPC pointers).  nseg == 0: the single buffer in/pitch/row0.
@@ -55,8 +62,8 @@ __host__ __device__ inline int slide_padded_words(int NC) {
 
 // Dynamic shared memory of the fast kernel: 2 padded prefix arrays, warp totals, 2*NS
 // mbarriers, and NS ring stages of (entering, leaving, centre) row segments of NC bytes.
-__host__ __device__ inline size_t slide_smem_bytes(int NC) {
-    return sizeof(uint32_t) * (2 * (size_t)slide_padded_words(NC) + 16) +
+__host__ __device__ inline size_t slide_smem_bytes(int NC, int PL) {
+    return sizeof(uint32_t) * (2 * (size_t)slide_padded_words(PL) + 16) +
            2 * SLIDE_STAGES * sizeof(uint64_t) + (size_t)SLIDE_STAGES * 3 * NC;
 }
 

@@ -103,3 +103,38 @@ def test_extreme_parameters_match_oracle(method, k, r, win):
     b, _ = engine.binarize(torch.from_numpy(wide).cuda(), win, method, k, r, want_tmap=False)
     assert np.array_equal(b.cpu().numpy(), oracle.binarize(wide, win, method, k, r, tmap=False,
                                                            threads=8)[0])
+
+
+@pytest.mark.parametrize("width", [1, 17, 500, 512, 1000, 2048, 2049, 2550, 4096])
+def test_edge_padded_single_strip(monkeypatch, width):
+    """slide_kernel's edge-padded layout (one strip = the image's own columns, no halo columns;
+    DTB_PAD=1 forces it wherever the image fits one strip): every window alignment class
+    (rx mod 4, rx mod 32 == 0), windows wider than the image, both methods, short bands."""
+    from paper_1210_3165_b200 import _lib
+    monkeypatch.setenv("DTB_PAD", "1")
+    monkeypatch.setenv("DTB_BB", "0")
+    rng = np.random.default_rng(width)
+    h = 150 if width > 1000 else 333
+    img = rng.integers(0, 256, (h, width)).astype(np.uint8)
+    img[: h // 3] = (img[: h // 3] // 64) + 120  # a near-flat region: ties and tiny variances
+    for win in (3, 5, 7, 9, 31, 63, 65, 127, 129, 255):
+        _check(img, win, "sauvola", 0.34)
+        assert _lib.lib().dtb_last_kernel().decode() == "slide_kernel"
+        _check(img, win, "niblack", -0.2)
+
+
+def test_edge_padded_batch_and_bands(monkeypatch):
+    torch = engine.torch_mod()
+    monkeypatch.setenv("DTB_PAD", "1")
+    imgs = np.stack([workloads.c3_image(i, size=512) for i in range(3)])
+    got = engine.binarize_batch(torch.from_numpy(imgs).cuda(), 31, "niblack", -0.2, 128.0)
+    for i in range(3):
+        want, _ = oracle.binarize(imgs[i], 31, "niblack", -0.2, tmap=False)
+        assert np.array_equal(got[i].cpu().numpy(), want)
+    img = workloads.c5_image()[:700, :1800]
+    dev = torch.from_numpy(img).cuda()
+    want, _ = oracle.binarize(img, 45, "sauvola", 0.5, tmap=False)
+    for y0, y1 in ((0, 1), (13, 400), (699, 700), (300, 700)):
+        a, z = max(y0 - 22, 0), min(y1 + 22, 700)
+        got = engine.binarize_band(dev[a:z], a, 700, y0, y1, 45, "sauvola", 0.5, 128.0)
+        assert np.array_equal(got.cpu().numpy(), want[y0:y1]), (y0, y1)
