@@ -1179,6 +1179,7 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         p.ncw = best_w;
         p.now = (best_tw + 32 * 32 - 1) / (32 * 32);
         p.NC = 1024 * best_w;
+        p.PL = p.NC;
         p.TW = best_tw;
         const int nt = 32 * (p.ncw + p.now);
         const size_t smem = ws_smem_bytes(p.NC);

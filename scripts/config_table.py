@@ -75,10 +75,16 @@ def audit(fn):
             "max_gap_of_would_flip": struct.unpack("<f", struct.pack("<I", gap & 0xFFFFFFFF))[0]}
 
 
-def row(name, px, ms, alg_bytes, exact, fn=None):
+def _lk():
+    from paper_1210_3165_b200 import _lib
+    return _lib.lib().dtb_last_kernel().decode()
+
+
+def row(name, px, ms, alg_bytes, exact, fn=None, kernel=None):
     from paper_1210_3165_b200 import _lib
     gbs = alg_bytes / (ms / 1e3) / 1e9
-    out = {"config": name, "kernel": _lib.lib().dtb_last_kernel().decode(), "pixels": int(px), "kernel_ms": round(ms, 4),
+    # dtb_last_kernel names the last BINARIZATION kernel: rows of other kernels pass theirs
+    out = {"config": name, "kernel": kernel or _lib.lib().dtb_last_kernel().decode(), "pixels": int(px), "kernel_ms": round(ms, 4),
            "mpix_per_s": round(px / (ms / 1e3) / 1e6, 1), "alg_bytes": int(alg_bytes),
            "achieved_gbs": round(gbs, 1), "roofline_frac": round(gbs / PEAK, 4),
            "bit_exact_vs_reference": exact}
@@ -111,7 +117,7 @@ def main():
     gray = engine.to_gray(rgb)
     ms = timed(lambda: engine.to_gray(rgb), a.reps)
     out.append(row("c2 to_gray 3508x2480", gray.numel(), ms, 4 * gray.numel(),
-                   sha(gray.cpu().numpy()) == GOLD["c2/rgb"]["gray"]))
+                   sha(gray.cpu().numpy()) == GOLD["c2/rgb"]["gray"], kernel="to_gray_kernel"))
     for w in cfg["c2"].windows:
         ms = timed(lambda: engine.binarize(gray, w, "sauvola", 0.5, 128.0, want_tmap=False), a.reps)
         b, _ = engine.binarize(gray, w, "sauvola", 0.5, 128.0, want_tmap=False)
@@ -121,7 +127,8 @@ def main():
         ms = timed(lambda: engine.rgb_binarize(rgb, w, "sauvola", 0.5, 128.0), a.reps)
         b = engine.rgb_binarize(rgb, w, "sauvola", 0.5, 128.0)
         out.append(row(f"c2 rgb->binary W{w}", gray.numel(), ms, 4 * gray.numel(),
-                       sha(b.cpu().numpy()) == GOLD[f"c2/w{w}"]["binary"]))
+                       sha(b.cpu().numpy()) == GOLD[f"c2/w{w}"]["binary"],
+                       kernel="to_gray_kernel + " + _lk()))
     del rgb, gray
     # C3 batch
     stack = torch.from_numpy(np.stack([workloads.c3_image(i) for i in range(64)])).cuda()

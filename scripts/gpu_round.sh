@@ -19,3 +19,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"bb_
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_ncu.log 2>&1; echo ncu=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"bb_kernel" -s 6 -c 1 -o $O/${TAG}_prof_band \
   python bench.py --emulate-bands 8 --steps 3 --warmup 3 > $O/${TAG}_ncu_band.log 2>&1; echo ncu_band=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"slide_kernel" -s 2 -c 1 -f -o $O/${TAG}_prof_c3 \
+  python scripts/c3_probe.py > $O/${TAG}_ncu_c3.log 2>&1; echo ncu_c3=$?
+timeout 300 python scripts/pad_probe.py > $O/${TAG}_pad_probe.log 2>&1; echo pad=$?
+timeout 1800 bash scripts/safety_checks.sh > $O/${TAG}_safety_checks.txt 2>&1; echo safety=$?
