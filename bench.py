@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
                     help="row-band halos: read in place from the neighbours' HBM (CUDA IPC, "
                          "fused into the kernel's row staging) or copied with NCCL send/recv")
+    ap.add_argument("--fresh-bands", action="store_true",
+                    help="N > 1, p2p halos: refill every band inside the step (device copy) and order "
+                         "the ranks with interprocess CUDA events (PeerHalos publish / retire) "
+                         "instead of timing constant bands")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -270,7 +274,14 @@ def run_ours(a):
         peers = None
         if use_p2p:
             try:
-                peers = [D.PeerHalos(bands[j], w["rows"], r) for j in range(nrot)]
+                hostg = None
+                if a.fresh_bands:  # host-only handshake group for the event hand-offs
+                    import torch.distributed as dist
+                    hostg = (dist.group.WORLD if dist.get_backend() == "gloo"
+                             else dist.new_group(backend="gloo"))
+                    band_src = band.clone()
+                peers = [D.PeerHalos(bands[j], w["rows"], r, events=a.fresh_bands, host_group=hostg)
+                         for j in range(nrot)]
                 peers[0].barrier()
             except (RuntimeError, ValueError) as exc:  # e.g. VMM allocations without IPC handles
                 if rank == 0:
@@ -281,7 +292,9 @@ def run_ours(a):
                                      device=dev) for _ in range(nrot)]
         w["halo_transport"] = ("none (1 GPU)" if world == 1 else
                      "read in place from the neighbours' HBM over NVLink (CUDA IPC), fused into "
-                     "the kernel's row staging" if use_p2p else "NCCL send/recv copy per step")
+                     "the kernel's row staging" + ("; bands refilled every step, ranks ordered by "
+                     "interprocess CUDA events" if a.fresh_bands else "")
+                     if use_p2p else "NCCL send/recv copy per step")
         launches_per_step = 1
 
         def kernel(i):
@@ -296,7 +309,11 @@ def run_ours(a):
             if use_p2p:
                 if ev is not None:
                     ev[0].record(stream)
-                peers[j].binarize(w["win"], w["method"], w["k"], w["r"], out=outs[j], sync=False)
+                if a.fresh_bands:  # new rows every step; ranks ordered on the device (IPC events)
+                    bands[j].copy_(band_src, non_blocking=True)
+                    peers[j].binarize(w["win"], w["method"], w["k"], w["r"], out=outs[j], sync="events")
+                else:
+                    peers[j].binarize(w["win"], w["method"], w["k"], w["r"], out=outs[j], sync=False)
                 if ev is not None:
                     ev[1].record(stream)
                 return

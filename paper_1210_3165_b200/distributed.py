@@ -170,9 +170,20 @@ class PeerHalos:
     any neighbour's kernel reads it (``binarize(sync=True)`` synchronises the stream and
     barriers the group first), and a rank must not overwrite its band until its
     neighbours' kernels are done (call ``barrier()`` after the step).
+
+    ``events=True`` adds device-side ordering for pipelines that refill the band every step:
+    each rank owns two interprocess CUDA events (band published / band consumed), exported
+    with ``cudaIpcGetEventHandle`` and opened by its neighbours.  ``publish()`` records the
+    first on the current stream and makes the stream wait on the neighbours' (so the kernel
+    that follows sees their new rows); ``retire()`` records the second after the kernel and
+    waits on the neighbours' (so the next refill cannot overtake a neighbour's kernel that
+    still reads this band).  ``cudaStreamWaitEvent`` captures the record that has been ISSUED
+    by the time it is called, so a host-only barrier over ``host_group`` (gloo: no device
+    work, no stream synchronisation) sits between record and wait; the GPU queue never drains.
     """
 
-    def __init__(self, band: torch.Tensor, rows: int, r: int, group=None):
+    def __init__(self, band: torch.Tensor, rows: int, r: int, group=None, events: bool = False,
+                 host_group=None):
         from . import engine
         self.group = group
         self.world = dist.get_world_size(group)
@@ -197,6 +208,23 @@ class PeerHalos:
                 base = engine.ipc_import(h)
                 self.mapped[nb] = base
                 self.addr[nb] = (base + off, pitch)
+        self.events = bool(events)
+        self.host_group = host_group if host_group is not None else group
+        if self.events:
+            if dist.get_backend(self.host_group) != "gloo":
+                raise ValueError("events: host_group must be a gloo group (host-only handshake)")
+            dev = band.device
+            self.ev_ready = torch.cuda.Event(enable_timing=False, interprocess=True)
+            self.ev_done = torch.cuda.Event(enable_timing=False, interprocess=True)
+            self.ev_ready.record()
+            self.ev_done.record()
+            evh = [None] * self.world
+            dist.all_gather_object(evh, (self.ev_ready.ipc_handle(), self.ev_done.ipc_handle()),
+                                   group=self.host_group)
+            self.nb_ready, self.nb_done = {}, {}
+            for nb in self.mapped:
+                self.nb_ready[nb] = torch.cuda.Event.from_ipc_handle(dev, evh[nb][0])
+                self.nb_done[nb] = torch.cuda.Event.from_ipc_handle(dev, evh[nb][1])
 
     def segments(self):
         """[(ptr, pitch, rows, cols)] for global rows [a, z) and the first global row a."""
@@ -214,15 +242,41 @@ class PeerHalos:
         torch.cuda.current_stream().synchronize()
         dist.barrier(group=self.group)
 
-    def binarize(self, win: int, method: str, k: float, r: float, out=None, sync: bool = True):
+    def _handoff(self, mine, theirs):
+        st = torch.cuda.current_stream()
+        mine.record(st)
+        dist.barrier(group=self.host_group)  # every rank has issued its record (host only)
+        for ev in theirs.values():
+            st.wait_event(ev)
+
+    def publish(self):
+        """The band's new contents are enqueued on the current stream: order the neighbours'
+        reads after them (and this rank's reads after the neighbours' refills)."""
+        self._handoff(self.ev_ready, self.nb_ready)
+
+    def retire(self):
+        """This rank's kernel is enqueued: order its next refill after the neighbours' kernels
+        that read this band."""
+        self._handoff(self.ev_done, self.nb_done)
+
+    def binarize(self, win: int, method: str, k: float, r: float, out=None, sync=True):
+        """``sync``: True = stream synchronise + group barrier first (one-shot use); False = the
+        caller orders the ranks; "events" = publish() / kernel / retire(), device-side."""
         from . import engine
         if win // 2 != self.r:
             raise ValueError(f"window: PeerHalos was built for r={self.r}, got W={win}")
-        if sync:
+        if sync == "events":
+            if not self.events:
+                raise ValueError("sync='events' needs PeerHalos(events=True)")
+            self.publish()
+        elif sync:
             self.barrier()
         segs, a = self.segments()
-        return engine.binarize_segments(segs, a, self.rows, self.y0, self.y1, win, method, k, r,
-                                        out=out)
+        res = engine.binarize_segments(segs, a, self.rows, self.y0, self.y1, win, method, k, r,
+                                       out=out)
+        if sync == "events":
+            self.retire()
+        return res
 
     def close(self):
         from . import engine

@@ -42,6 +42,13 @@ def test_bench_two_ranks_p2p(cfg):
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 2
 
 
+def test_bench_two_ranks_fresh_bands_event_ordering():
+    d = _torchrun(["--config", "c5", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
+                   "--fresh-bands"], {})
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert "interprocess CUDA events" in d["config"]["halo"]
+
+
 def test_bench_reference_arm_two_ranks():
     d = _torchrun(["--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "3"], {})
     assert d["impl"] == "reference" and d["value"] > 0

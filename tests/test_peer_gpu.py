@@ -107,6 +107,63 @@ def test_peer_halos_across_processes(world, rows, cols, win):
     page = torch.from_numpy(_page(rows, cols, seed=11)).cuda()
     want, _ = engine.binarize(page, win, "sauvola", 0.34, 128.0, want_tmap=False)
     want = want.cpu().numpy()
+    import oracle
+    want_cpu, _ = oracle.binarize(_page(rows, cols, seed=11), win, "sauvola", 0.34, 128.0, tmap=False)
+    assert np.array_equal(want, want_cpu)  # the multi-process bands are pinned to the oracle too
     for rank, y0, y1, res, res2 in got:
         assert np.array_equal(res, want[y0:y1]), rank
         assert np.array_equal(res2, want[y0:y1]), rank
+
+
+def _rank_events(rank, world, port, rows, cols, win, steps, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        y0, y1 = D.band_bounds(rows, world, rank)
+        band = torch.zeros((y1 - y0, cols), dtype=torch.uint8, device="cuda")
+        ph = D.PeerHalos(band, rows, win // 2, events=True)
+        fresh = [torch.from_numpy(np.ascontiguousarray(_page(rows, cols, seed=20 + s)[y0:y1])).cuda()
+                 for s in range(steps)]
+        outs = [torch.empty_like(band) for _ in range(steps)]
+        torch.cuda.synchronize()
+        dist.barrier()
+        # every step refills the band on the stream and binarizes it; ranks are ordered by the
+        # interprocess events only (no stream synchronisation inside the loop)
+        for s in range(steps):
+            band.copy_(fresh[s], non_blocking=True)
+            ph.binarize(win, "sauvola", 0.34, 128.0, out=outs[s], sync="events")
+        torch.cuda.synchronize()
+        dist.barrier()
+        ph.close()
+        q.put((rank, y0, y1, [o.cpu().numpy() for o in outs]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,rows,cols,win", [(2, 600, 1536, 127), (3, 450, 1024, 31)])
+def test_peer_halos_device_side_ordering(world, rows, cols, win):
+    """Fresh bands every step, ranks ordered by interprocess CUDA events (publish / retire)
+    instead of a stream synchronise + barrier: every step of every rank must equal the whole
+    page of that step, against the CPU oracle as well as the GPU whole-page result."""
+    import oracle
+    import torch.multiprocessing as mp
+    steps = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_events, args=(i, world, port, rows, cols, win, steps, q))
+             for i in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for s in range(steps):
+        page = _page(rows, cols, seed=20 + s)
+        want, _ = oracle.binarize(page, win, "sauvola", 0.34, 128.0, tmap=False)
+        for rank, y0, y1, outs in got:
+            assert np.array_equal(outs[s], want[y0:y1]), (s, rank)
