@@ -96,6 +96,9 @@ def cpu_model() -> str:
 
 DTYPE = ("u8 in/out; exact uint32 window sums; decision from certified fp32 bounds "
          "(8-pixel groups, then per pixel), fp64 reference replay of undecided pixels")
+# the per-pixel kernels (slide_kernel / ws_kernel: Niblack, small windows, small pages)
+DTYPE_PIXEL = ("u8 in/out; exact uint32 window sums; per-pixel decision from a certified fp32 "
+               "threshold, fp64 reference replay of pixels within the certified tolerance")
 
 
 def measured_peaks():
@@ -159,6 +162,61 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+class NvmlSampler:
+    """SM clock + clock-event (throttle) reasons read through NVML every ~2 ms by a thread while
+    the timed region runs (the timed region of the default run is ~20 ms: nvidia-smi's fastest
+    loop, 50 ms, gives it one sample).  NVML calls release the GIL; timing is by CUDA events."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
+
+    def __init__(self, device_index: int):
+        import pynvml
+        import torch
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+        try:
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid).encode())
+        except Exception:
+            self.h = pynvml.nvmlDeviceGetHandleByUUID("GPU-" + uuid)
+        self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)  # fail here, not in the thread
+        self.lines = []  # (sm MHz, reasons bitmask); cleared at the start of the timed region
+        self.run = True
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
+
+    def _loop(self):
+        nv = self.nv
+        while self.run:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+                except Exception:
+                    rs = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+                self.lines.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def stop(self):
+        self.run = False
+        self.t.join(timeout=2)
+        sm = [a for a, _ in self.lines]
+        reasons = sorted({name for _, rs in self.lines for bit, name in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.mx,
+                "reasons": reasons, "samples": len(sm), "source": "nvml, 2 ms period"}
+
+
+def clock_sampler(device_index: int):
+    try:
+        return NvmlSampler(device_index)
+    except Exception:
+        return ClockSampler(None)
 
 
 # ----------------------------------------------------------------------------- workloads
@@ -361,7 +419,7 @@ def run_ours(a):
             else:
                 dist.barrier()
 
-    sampler = ClockSampler(None) if rank == 0 else None
+    sampler = clock_sampler(local) if rank == 0 else None
     for i in range(a.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -369,10 +427,10 @@ def run_ours(a):
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(a.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if sampler:
-        sampler.lines.clear()  # keep only samples taken during the timed region
     barrier()
     torch.cuda.synchronize()
+    if sampler:
+        sampler.lines.clear()  # keep only samples taken during the timed region
     t0.record(stream)
     for i in range(a.steps):
         step(i, kev[i])
@@ -426,7 +484,7 @@ def run_ours(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 5),
             "higher_is_better": True,
             "scaling": a.scaling if w["kind"] != "rgb" else "weak",
-            "vs_baseline": None, "dtype": DTYPE,
+            "vs_baseline": None, "dtype": DTYPE if kernel_name == "bb_kernel" else DTYPE_PIXEL,
             "data": "synthetic (seeded, paper_1210_3165_b200/workloads.py)",
             "config": {"workload": w["desc"], "image": w["shape"], "window": w["win"],
                        "method": w["method"], "k": w["k"], "r": w["r"],
