@@ -280,13 +280,17 @@ __device__ __forceinline__ void row_outputs_tmap(const uint32_t* sPS, const uint
 }
 
 // register budget: V=16 fits 128 registers without spills (4 CTAs x 4 warps per SM)
-#ifndef DTB_SLIDE_MINB
-#define DTB_SLIDE_MINB(V) ((V) == 16 ? 2 : 1)
+// V = 16: 128 registers (4 CTAs x 4 warps per SM); the plain Niblack variant fits 96 without
+// spills, which makes room for a fifth 4-warp CTA (C3 0.670 -> 0.640 ms; the Sauvola variants
+// measured 1-2% slower at 96 / 104 / 112 on C5 and C2 and stay at 128)
+#ifndef DTB_SLIDE_MAXREG16_NIBLACK
+#define DTB_SLIDE_MAXREG16_NIBLACK 96
 #endif
 
 // MX = method code | 4 for the segmented-input variant (dtb_binarize_segments)
 template <int V, int RXM4, int MX>
-__global__ void __launch_bounds__(256, DTB_SLIDE_MINB(V)) slide_kernel(SlideParams p) {
+__global__ void __maxnreg__(V == 32 ? 255 : (MX == DTB_METHOD_NIBLACK ? DTB_SLIDE_MAXREG16_NIBLACK : 128))
+slide_kernel(SlideParams p) {
     constexpr int METHOD = MX & 3;
     constexpr bool SEG = (MX & 4) != 0;
     constexpr bool TMAP = (MX & 8) != 0;  // also write the fp64 threshold map (exact per pixel)
