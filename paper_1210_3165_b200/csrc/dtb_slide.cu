@@ -1157,7 +1157,15 @@ cudaError_t launch_slide(SlideParams p, int n_images, int num_sms, cudaStream_t 
         const int Vp = 16;
         const int wp = (p.cols + 32 * Vp - 1) / (32 * Vp);
         const long workp = 32L * Vp * wp;
-        if (wp <= 8 && (pad_mode() == 1 || best_w == 0 || workp * 10 <= pl.work * 9)) {
+        // the halo plan it competes with: the V = 16 one where the rule below would take it
+        // (C2's 2480-wide page is one 2560-column strip either way and stays on the halo layout,
+        // measured 1-4% faster there)
+        long halo_work = pl.work;
+        if (!p.tmap && V == 32) {
+            const Plan h16 = plan_for(16);
+            if (h16.w > 0 && (pl.w == 0 || h16.work * 10 <= pl.work * 9)) halo_work = h16.work;
+        }
+        if (wp <= 8 && (pad_mode() == 1 || best_w == 0 || workp * 10 <= halo_work * 9)) {
             V = Vp;
             p.pad = 32 * ((p.rx + 31) / 32);
             p.padr = 4 * ((p.rx + 4) / 4 + 1);

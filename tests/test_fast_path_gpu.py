@@ -138,3 +138,28 @@ def test_edge_padded_batch_and_bands(monkeypatch):
         a, z = max(y0 - 22, 0), min(y1 + 22, 700)
         got = engine.binarize_band(dev[a:z], a, 700, y0, y1, 45, "sauvola", 0.5, 128.0)
         assert np.array_equal(got.cpu().numpy(), want[y0:y1]), (y0, y1)
+
+
+def test_planner_takes_the_edge_padded_strip_when_it_saves_columns():
+    """Default planner rule (DTB_PAD unset): a 2048-wide page at W31 runs one edge-padded strip
+    (5 x 512 halo columns -> 2048), C2's 2480-wide page keeps the halo layout (one 2560-column
+    strip either way).
+    The plan is read from DTB_PRINT_PLAN's stderr line in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import numpy as np, torch\n"
+            "from paper_1210_3165_b200 import engine\n"
+            "for w in (2048, 2480):\n"
+            "    img = np.random.default_rng(w).integers(0, 256, (64, w)).astype(np.uint8)\n"
+            "    engine.binarize(img, 31, 'niblack', -0.2, 128.0, want_tmap=False)\n"
+            "torch.cuda.synchronize()\n")
+    env = dict(os.environ, DTB_PRINT_PLAN="1")
+    env.pop("DTB_PAD", None)
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                         cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stderr[-2000:]
+    plans = [ln for ln in res.stderr.splitlines() if ln.startswith("[dtb plan] slide_kernel")]
+    assert any("cols=2048" in ln and "strips=1" in ln and "pad=32" in ln for ln in plans), plans
+    assert any("cols=2480" in ln and "pad=0" in ln for ln in plans), plans
