@@ -21,15 +21,18 @@ from . import _lib
 METHOD_CODES = {"sauvola": _lib.DTB_METHOD_SAUVOLA, "niblack": _lib.DTB_METHOD_NIBLACK}
 
 _torch = None
+_cuda_ok = False  # set by the first successful availability check (it costs ~3 us a call)
 
 
 def torch_mod():
-    global _torch
+    global _torch, _cuda_ok
     if _torch is None:
         import torch
         _torch = torch
-    if not _torch.cuda.is_available():
-        raise RuntimeError("paper_1210_3165_b200 needs a CUDA device (there is no CPU fallback)")
+    if not _cuda_ok:
+        if not _torch.cuda.is_available():
+            raise RuntimeError("paper_1210_3165_b200 needs a CUDA device (there is no CPU fallback)")
+        _cuda_ok = True
     return _torch
 
 
